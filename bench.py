@@ -1,0 +1,299 @@
+#!/usr/bin/env python
+"""Benchmark of the PaSE strategy-search hot path on B200 (contract: see DESIGN.md §7).
+
+One STEP = one complete search (pase_solve: cost tables, DP fill over the elimination
+tree, back-substitution, strategy to host) of the workload named in config.workload.
+  value  = DP entries/s = candidates per search (sum_i K(sigma_i)|T(i)|)
+           x steps / device time of the timed steps (CUDA events on the library stream),
+           graph descriptors already resident in HBM (pase_create done before timing).
+  e2e    = the same metric through the public API with host inputs: pase_create (graph
+           from host memory, descriptors H2D) + pase_solve (strategy D2H) + pase_destroy.
+Default workload: Transformer 6+6, d_model 1024, p = 64 simulated devices, EXACT_P
+(BASELINE.json configs[4], the north-star config).  L2 is flushed (256 MiB write)
+before every timed step.
+
+--impl reference runs the CPU oracle (oracle/, the reference arm of this tier) on the
+host cores for the same workload and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (zoo builder key, p, policy, description)
+    "transformer": ("transformer", 64, "exact_p", "Transformer 6+6 d_model 1024 (b64 s256 h16 ff4096 v32768), p=64, EXACT_P"),
+    "transformer_le": ("transformer", 64, "le_p", "Transformer 6+6 d_model 1024, p=64, LE_P (prod <= p)"),
+    "inception_v3": ("inception_v3", 32, "exact_p", "InceptionV3 218 vertices, b128, p=32, EXACT_P"),
+    "gnmt": ("gnmt", 64, "exact_p", "GNMT unrolled 2+2 layers x 40 steps, p=64, EXACT_P"),
+    "gnmt_le": ("gnmt", 64, "le_p", "GNMT unrolled 2+2 layers x 40 steps, p=64, LE_P"),
+    "rnnlm": ("rnnlm", 64, "exact_p", "RNNLM unrolled 2 layers x 40 steps, p=64, EXACT_P"),
+    "alexnet": ("alexnet", 8, "exact_p", "AlexNet b128, p=8, EXACT_P"),
+    "mlp": ("mlp", 4, "exact_p", "4-layer MLP b64 h256, p=4, EXACT_P"),
+}
+SM_COUNT = 148
+FP64_LANES_PER_SM = 64          # B200 fp64 pipe, 37 TFLOP/s (FMA=2) / 148 SM / 1.965 GHz / 2
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                                      "--query-gpu=" + ",".join(self.FIELDS), "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                parts = [x.strip() for x in out.split(",")]
+                if len(parts) == len(self.FIELDS):
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[k] for s in self.samples for k in range(4) if s[2 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def oracle_solve(graph, p, policy, threads):
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    P = O.Problem.from_model(graph, p, O.EXACT_P if policy == "exact_p" else O.LE_P)
+    r = P.dp(threads=threads)
+    return time.perf_counter() - t0, r, P
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from paper_2407_04001_b200 import zoo
+    key, p, policy, desc = WORKLOADS[args.workload]
+    g = zoo.bench_graph(key)[0]
+    threads = os.cpu_count() or 1
+    from oracle import oracle as O
+    cand = None
+    for _ in range(args.warmup):
+        dt, r, P = oracle_solve(g, p, policy, threads)
+    times = []
+    for _ in range(args.steps):
+        dt, r, P = oracle_solve(g, p, policy, threads)
+        times.append(dt)
+        if cand is None:
+            cand = P.table_sizes()[1]
+    if cand is None:
+        dt, r, P = oracle_solve(g, p, policy, threads)
+        cand = P.table_sizes()[1]
+    tot = sum(times)
+    value = cand * len(times) / tot
+    line = {
+        "impl": "reference", "metric": "DP entries/s (strategy search, PaSE Eq. 4 / Fig. 5)",
+        "value": value, "unit": "entries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "p": p, "policy": policy, "candidates": cand},
+        "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "oracle",
+                         "sample": "full workload, one complete search per step (cost tables + Fig. 5 DP)"},
+        "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="transformer", choices=sorted(WORKLOADS))
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--flush-mb", type=int, default=256)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    from paper_2407_04001_b200 import pase, zoo
+    torch.cuda.set_device(local_rank)
+    dist = None
+    uid = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        buf = [pase.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(buf, src=0)
+        uid = buf[0]
+    key, p, policy, desc = WORKLOADS[args.workload]
+    graph = zoo.bench_graph(key)[0]
+    stream = torch.cuda.Stream()
+    flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device="cuda")
+
+    ctx = pase.Context(graph, p, policy=policy, device=local_rank, stream=stream.cuda_stream,
+                       rank=rank, world=world, uid=uid)
+    st0 = ctx.stats()
+    cand = int(st0["candidates"])
+    for _ in range(args.warmup):
+        ctx.solve()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    step_ms, dp_ms, tab_ms = [], [], []
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)                              # L2 flush outside the timed events
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = ctx.solve()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            s = ctx.stats()
+            dp_ms.append(s["ms_dp"])
+            tab_ms.append(s["ms_tables"])
+        barrier()
+        time.sleep(0.25)
+    tot_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = cand * args.steps / (tot_ms / 1e3)
+    st = ctx.stats()
+    ctx.close()
+
+    # e2e through the public API with host inputs (create + solve + destroy per step)
+    e2e_ms = []
+    for i in range(args.e2e_steps + 1):
+        with torch.cuda.stream(stream):
+            flush.fill_(1)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        with pase.Context(graph, p, policy=policy, device=local_rank, stream=stream.cuda_stream,
+                          rank=rank, world=world, uid=uid) as c2:
+            c2.solve()
+        e1.record(stream)
+        e1.synchronize()
+        if i > 0:                                   # first one warms host caches
+            e2e_ms.append(e0.elapsed_time(e1))
+    e2e_tot = sum(e2e_ms)
+    if dist is not None:
+        t = torch.tensor([e2e_tot], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_tot = float(t.item())
+    e2e_value = cand * len(e2e_ms) / (e2e_tot / 1e3)
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return 0
+    peaks = load_peaks()
+    clocks = clk.summary()
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    fp64_peak = SM_COUNT * FP64_LANES_PER_SM * sm_mhz * 1e6 / 1e12          # Tops/s
+    mean_dp = statistics.mean(dp_ms)
+    achieved = st["dp_fp64_ops"] / (mean_dp / 1e3) / 1e12
+    hbm_peak = peaks.get("hbm_gbs", 6538.0)
+    hbm_achieved = st["alg_bytes_dp"] / (mean_dp / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(args.workload)
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        threads = os.cpu_count() or 1
+        dt, r_or, P = oracle_solve(graph, p, policy, threads)
+        cpu = {"value": cand / dt, "unit": "entries/s", "cores": threads, "kind": "oracle",
+               "sample": f"full workload, one complete search ({dt:.2f} s: cost tables + Fig. 5 DP)",
+               "parity": bool(list(r_or["strategy"]) == list(r["config_index"]) and r_or["cost"] == r["cost"])}
+    line = {
+        "metric": "DP entries/s (strategy search, PaSE Eq. 4 / Fig. 5)",
+        "value": value, "unit": "entries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "p": p, "policy": policy, "vertices": st["n_vertices"],
+                   "candidates": cand, "table_entries": int(st["table_entries"]), "M": st["max_dep"],
+                   "K": st["max_configs"], "tree_levels": st["tree_levels"],
+                   "l2": f"flushed ({args.flush_mb} MiB write) before every timed step",
+                   "parallelism": f"dp-table partition over {world} GPU(s)"},
+        "phases_ms": {"tables": statistics.mean(tab_ms), "dp_fill": mean_dp,
+                      "solve_total": statistics.mean(step_ms)},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp64_peak, "traffic": traffic,
+                     "kernel": "dp_fill (all launches of the DP phase, CUDA events in the solve graph)",
+                     "peak_source": f"derived: {SM_COUNT} SM x {FP64_LANES_PER_SM} fp64 lanes x {sm_mhz:.0f} MHz (DESIGN §5)",
+                     "hbm_view": {"achieved_gbs": hbm_achieved, "peak_gbs": hbm_peak,
+                                  "frac": hbm_achieved / hbm_peak, "alg_bytes": int(st["alg_bytes_dp"])}},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "entries/s", "h2d_bytes_per_step": int(st["h2d_bytes"]),
+                "d2h_bytes_per_step": int(st["d2h_bytes"]), "ms_per_step": e2e_tot / max(len(e2e_ms), 1),
+                "what": "pase_create (host graph -> plan -> H2D) + pase_solve (D2H strategy) + pase_destroy"},
+        "gpu_launches": int(st["n_launches"]) * args.steps,
+        "clocks": clocks,
+        "paper_context": "PaSE Table 1 (PAPER.md:753-762): Transformer p=64 search 1883.187 s, Python on Xeon E5; dims unpublished",
+    }
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,183 @@
+/*
+ * pase.h -- C ABI of the B200-native PaSE strategy-search hot path
+ * ("PaSE: Parallelization Strategies for Efficient DNN Training", arXiv 2407.04001).
+ *
+ * Citation convention: P:<n> = /root/reference/PAPER.md line n (section / equation /
+ * figure named alongside).  DESIGN.md §2 lists every reading of an ambiguous passage.
+ *
+ * What the library computes (one call to pase_solve = the whole hot path):
+ *   a1 graph ingest/validation       G = (V, E), weakly connected (§2)
+ *   a2 configurations C(v)           d-tuples, c_k | size_k, prod c_k = p
+ *   a3 SortNodes + D(i)              Fig. 4
+ *   a4 elimination tree              children(i) = {j : min-rank D(j) = i}; equals Fig. 5's
+ *                                    connected subsets S(i)
+ *   a5 cost tables (GPU)             L_v[C] = t_l(v,C,r); W_e = r*t_x (Eq. 1)
+ *   a6 DP fill (GPU)                 Eq. 4 / Fig. 5 lines 8-20:
+ *                                    T(i)[phi] = min_C L[C] + sum_{e in E>(sigma_i)} W_e + sum_j T(j)[phi'|D(j)]
+ *   a7 back-substitution (GPU)       from sigma_|V|.cfg
+ *   a8 total cost                    f(|V|, ∅) = T(|V|)[0]
+ *
+ * Conventions for every entry point:
+ *   - all functions are extern "C", never throw, and return pase_status;
+ *   - pointers are HOST pointers unless the name ends in _dev;
+ *   - caller-allocated outputs; the library never retains caller pointers after return;
+ *   - a pase_ctx is not thread-safe; distinct contexts are independent.
+ *   - errors: PASE_ERR_INVALID (bad input; message names the node / edge), PASE_ERR_RESOURCE
+ *     (size guard or allocation failure; message carries M and K, cf. Table 1 "OOM"),
+ *     PASE_ERR_CUDA / PASE_ERR_NCCL (runtime failures), PASE_ERR_STATE (call out of order).
+ *     pase_last_error(ctx) returns the message (valid until the next call on ctx);
+ *     pase_last_error(NULL) returns the message of the last failed pase_create.
+ */
+#ifndef PASE_H
+#define PASE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PASE_MAX_DIMS 8      /* iteration-space dimensions per vertex */
+#define PASE_MAX_HALO 4      /* conv halo (spatial, filter) pairs per vertex */
+#define PASE_MAX_DEP 12      /* max |D(i)| (M); larger -> PASE_ERR_RESOURCE */
+#define PASE_UID_BYTES 128   /* ncclUniqueId size */
+
+typedef enum {
+    PASE_OK = 0,
+    PASE_ERR_INVALID = 1,
+    PASE_ERR_RESOURCE = 2,
+    PASE_ERR_CUDA = 3,
+    PASE_ERR_NCCL = 4,
+    PASE_ERR_STATE = 5
+} pase_status;
+
+/* C(v) policy (DESIGN reading B).  Both require c_k | size_k ("equal parts").
+ * EXACT_P: prod c_k = p (north star); if no tuple reaches p, the tuples of the largest
+ * achievable product <= p.  LE_P: prod c_k <= p (the set-builder of P:204-205). */
+typedef enum { PASE_CFG_EXACT_P = 0, PASE_CFG_LE_P = 1 } pase_cfg_policy;
+
+/* One vertex = one layer with its iteration space. */
+typedef struct {
+    int32_t n_dims;                        /* 1..PASE_MAX_DIMS */
+    int64_t size[PASE_MAX_DIMS];           /* extents, >= 1 */
+    uint32_t splittable_mask;              /* bit k: dim k may be split */
+    int32_t n_out_axes;                    /* output tensor rank, 1..n_dims */
+    int32_t out_axes[PASE_MAX_DIMS];       /* iteration dim of each output-tensor axis (distinct) */
+    int32_t n_w_axes;                      /* 0 = no weight */
+    int32_t w_axes[PASE_MAX_DIMS];         /* iteration dims indexing the weight (distinct) */
+    uint32_t flop_dims_mask;               /* dims in the FLOP product; 0 = all dims */
+    int64_t flops_per_point;               /* fwd+bwd FLOPs per iteration point (e.g. 6 for GEMM) */
+    int32_t n_halo;                        /* 0..PASE_MAX_HALO */
+    int32_t halo_spatial[PASE_MAX_HALO];   /* spatial iteration dim h ... */
+    int32_t halo_filter[PASE_MAX_HALO];    /* ... paired with filter dim r */
+    int32_t elem_bytes;                    /* bytes per tensor element, >= 1 */
+} pase_node;
+
+/* Tensor flowing src -> dst.  axis_map[a] = dst iteration dim aligned with
+ * src output axis a (a < src.n_out_axes), or -1 (consumer does not split it). */
+typedef struct {
+    int32_t src, dst;
+    int32_t axis_map[PASE_MAX_DIMS];
+} pase_edge;
+
+typedef struct {
+    int32_t n_nodes;
+    const pase_node* nodes;    /* node id = index */
+    int32_t n_edges;
+    const pase_edge* edges;    /* edge id = index; parallel / antiparallel edges allowed */
+} pase_graph;
+
+/* Machine model: r = F / B computed once in fp64. */
+typedef struct {
+    double flops_per_device;           /* F, FLOP/s */
+    double link_bandwidth;             /* B, bytes/s (may be +inf: r = 0) */
+    int32_t cfg_policy;                /* pase_cfg_policy */
+    int32_t reserved0;
+    uint64_t table_budget_bytes;       /* size guard over all DP tables; 0 = 64 GiB */
+    uint64_t redundant_below_bytes;    /* multi-GPU: tables below this are computed on every rank */
+    int32_t cuda_device;               /* device ordinal for this process; < 0 = host-only planning
+                                          context (a1-a4 + stats + introspection; pase_solve and the
+                                          table hooks return PASE_ERR_STATE; no device is touched) */
+    int32_t rank, world;               /* search GPUs G (1, 2, 4, 8); world = 1: single GPU */
+    int32_t reserved1;
+    const void* nccl_unique_id;        /* PASE_UID_BYTES bytes, same on every rank; NULL if world == 1 */
+    void* cuda_stream;                 /* cudaStream_t to run on; NULL = library-owned stream */
+} pase_machine;
+
+typedef struct {
+    int32_t n_vertices, n_edges;
+    int32_t max_dep;                   /* M = max |D(i)| */
+    int32_t max_configs;               /* K = max |C(v)| */
+    int32_t tree_levels;               /* elimination-tree depth */
+    int32_t n_launches;                /* kernels launched per pase_solve */
+    uint64_t candidates;               /* sum_i K(sigma_i) * |T(i)|  ("combinations") */
+    uint64_t table_entries;            /* sum_i |T(i)| */
+    uint64_t cost_entries;             /* sum_v K_v + sum_e K_u K_v */
+    uint64_t alg_bytes_dp;             /* algorithmic HBM bytes of the DP fill */
+    uint64_t alg_bytes_tables;         /* bytes written by the cost-table kernel */
+    uint64_t comm_bytes;               /* multi-GPU all-gather bytes per solve (this rank) */
+    double ms_create;                  /* host: ingest..plan..alloc (excl. NCCL init) */
+    double ms_nccl_init;
+    double ms_solve;                   /* device time of the last pase_solve (CUDA events) */
+    double ms_tables, ms_dp;           /* phase split of the last pase_solve (CUDA events in the graph) */
+    uint64_t dp_fp64_ops;              /* sum_i N_i * (terms_i - 1 adds + 1 compare) of the DP fill */
+    uint64_t h2d_bytes;                /* bytes copied host->device by pase_create */
+    uint64_t d2h_bytes;                /* bytes copied device->host per pase_solve */
+} pase_stats;
+
+typedef struct pase_ctx pase_ctx;
+
+/* a1-a4 + allocation: validates and deep-copies g (caller may free it on return), enumerates
+ * C(v), runs SortNodes, builds the elimination tree, plans table layouts, applies the size
+ * guard, allocates device memory on m->cuda_device and records the solve schedule as a
+ * CUDA graph.  p >= 1 is the simulated device count.  *out is NULL on failure. */
+pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, pase_ctx** out);
+
+/* a5-a8: runs the whole search on the GPU (cost tables, DP fill over the elimination tree,
+ * back-substitution).  configs_out: caller-allocated int32[n_nodes * PASE_MAX_DIMS], row v =
+ * the split tuple of node v (unused dims = 1); may be NULL.  config_index_out: int32[n_nodes]
+ * index of phi*(v) in C(v) (lexicographic order); may be NULL.  total_cost_out: f(|V|, ∅).
+ * May be called repeatedly; every call recomputes everything. */
+pase_status pase_solve(pase_ctx* ctx, int32_t* configs_out, int32_t* config_index_out,
+                       double* total_cost_out);
+
+pase_status pase_get_stats(const pase_ctx* ctx, pase_stats* out);
+const char* pase_last_error(const pase_ctx* ctx);
+void pase_destroy(pase_ctx* ctx);   /* NULL-safe; frees device memory, graph, comm */
+
+/* ---- introspection / test hooks (host pointers, caller-allocated) -------------------- */
+
+/* counts[n_nodes] = |C(v)|; tuples (may be NULL) = per node in id order, counts[v] rows of
+ * PASE_MAX_DIMS int32 (unused dims = 1), lexicographic (dim 0 most significant). */
+pase_status pase_get_configs(const pase_ctx* ctx, int32_t* counts, int32_t* tuples);
+
+/* sigma[n] (rank -> node), dep_off[n+1] / dep_ids[<= n*PASE_MAX_DEP] = D(i) ascending rank,
+ * parent[n] = rank of min-rank D(i) (-1 for the root).  Any pointer may be NULL. */
+pase_status pase_get_order(const pase_ctx* ctx, int32_t* sigma, int32_t* dep_off,
+                           int32_t* dep_ids, int32_t* parent);
+
+/* Cost tables of the last pase_solve, in the ORACLE layout: is_edge = 0: L_v[K_v];
+ * is_edge = 1: W_e[c_src * K_dst + c_dst] (already multiplied by r). */
+pase_status pase_get_cost_tables(const pase_ctx* ctx, int32_t index, int32_t is_edge, double* out);
+
+/* T(i) and A(i) of rank i after pase_solve (|T(i)| entries; coordinates D(i) ascending rank,
+ * lowest rank fastest).  On multi-GPU contexts the partitions are gathered. */
+pase_status pase_get_dp_table(const pase_ctx* ctx, int32_t rank, double* T_out, uint16_t* A_out);
+int64_t pase_table_entries(const pase_ctx* ctx, int32_t rank);
+
+/* Replace the cost model by explicit tables (synthetic-cost tests): L concatenated
+ * over nodes in id order (K_v each), W over edges in id order (K_src*K_dst each, src-major).
+ * Subsequent pase_solve calls use these tables instead of running the cost-table kernel. */
+pase_status pase_set_cost_tables(pase_ctx* ctx, const double* L, const double* W);
+
+/* Time the solve phases separately on the next pase_solve (adds syncs; default off). */
+pase_status pase_set_profiling(pase_ctx* ctx, int32_t enable);
+
+/* NCCL unique id for multi-GPU contexts (rank 0 calls it and broadcasts the bytes). */
+pase_status pase_get_unique_id(void* uid_out /* PASE_UID_BYTES */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PASE_H */

@@ -1,0 +1,344 @@
+"""Thin ctypes binding of libpase.so (include/pase.h).  Argument marshalling only: every
+step of the search runs inside the library (host C++ + sm_100a kernels).  There is no
+CPU fallback: if libpase.so is missing or no CUDA device is present, calls fail loudly.
+
+The names mirror the C ABI: pase_create / pase_solve / pase_get_stats / ... plus a
+convenience ``solve(graph, p, ...)``.  Graphs are the dicts of ``zoo.py``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libpase.so")
+
+PASE_MAX_DIMS = 8
+PASE_MAX_HALO = 4
+PASE_MAX_DEP = 12
+PASE_UID_BYTES = 128
+PASE_CFG_EXACT_P, PASE_CFG_LE_P = 0, 1
+STATUS = {0: "PASE_OK", 1: "PASE_ERR_INVALID", 2: "PASE_ERR_RESOURCE", 3: "PASE_ERR_CUDA",
+          4: "PASE_ERR_NCCL", 5: "PASE_ERR_STATE"}
+POLICIES = {"exact_p": PASE_CFG_EXACT_P, "le_p": PASE_CFG_LE_P}
+
+
+class pase_node(C.Structure):
+    _fields_ = [
+        ("n_dims", C.c_int32),
+        ("size", C.c_int64 * PASE_MAX_DIMS),
+        ("splittable_mask", C.c_uint32),
+        ("n_out_axes", C.c_int32),
+        ("out_axes", C.c_int32 * PASE_MAX_DIMS),
+        ("n_w_axes", C.c_int32),
+        ("w_axes", C.c_int32 * PASE_MAX_DIMS),
+        ("flop_dims_mask", C.c_uint32),
+        ("flops_per_point", C.c_int64),
+        ("n_halo", C.c_int32),
+        ("halo_spatial", C.c_int32 * PASE_MAX_HALO),
+        ("halo_filter", C.c_int32 * PASE_MAX_HALO),
+        ("elem_bytes", C.c_int32),
+    ]
+
+
+class pase_edge(C.Structure):
+    _fields_ = [("src", C.c_int32), ("dst", C.c_int32), ("axis_map", C.c_int32 * PASE_MAX_DIMS)]
+
+
+class pase_graph(C.Structure):
+    _fields_ = [("n_nodes", C.c_int32), ("nodes", C.POINTER(pase_node)),
+                ("n_edges", C.c_int32), ("edges", C.POINTER(pase_edge))]
+
+
+class pase_machine(C.Structure):
+    _fields_ = [
+        ("flops_per_device", C.c_double),
+        ("link_bandwidth", C.c_double),
+        ("cfg_policy", C.c_int32),
+        ("reserved0", C.c_int32),
+        ("table_budget_bytes", C.c_uint64),
+        ("redundant_below_bytes", C.c_uint64),
+        ("cuda_device", C.c_int32),
+        ("rank", C.c_int32),
+        ("world", C.c_int32),
+        ("reserved1", C.c_int32),
+        ("nccl_unique_id", C.c_void_p),
+        ("cuda_stream", C.c_void_p),
+    ]
+
+
+class pase_stats(C.Structure):
+    _fields_ = [
+        ("n_vertices", C.c_int32), ("n_edges", C.c_int32),
+        ("max_dep", C.c_int32), ("max_configs", C.c_int32),
+        ("tree_levels", C.c_int32), ("n_launches", C.c_int32),
+        ("candidates", C.c_uint64), ("table_entries", C.c_uint64),
+        ("cost_entries", C.c_uint64), ("alg_bytes_dp", C.c_uint64),
+        ("alg_bytes_tables", C.c_uint64), ("comm_bytes", C.c_uint64),
+        ("ms_create", C.c_double), ("ms_nccl_init", C.c_double),
+        ("ms_solve", C.c_double), ("ms_tables", C.c_double), ("ms_dp", C.c_double),
+        ("dp_fp64_ops", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+    ]
+
+
+EXPORTS = ["pase_create", "pase_solve", "pase_get_stats", "pase_last_error", "pase_destroy",
+           "pase_get_configs", "pase_get_order", "pase_get_cost_tables", "pase_get_dp_table",
+           "pase_table_entries", "pase_set_cost_tables", "pase_set_profiling", "pase_get_unique_id"]
+
+_lib = None
+
+
+class PaseError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def load(path: str = SO):
+    """Load libpase.so (no fallback: a missing library is an error)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(path)
+    P = C.POINTER
+    ctx_p = C.c_void_p
+    L.pase_create.argtypes = [P(pase_graph), C.c_int32, P(pase_machine), P(ctx_p)]
+    L.pase_solve.argtypes = [ctx_p, P(C.c_int32), P(C.c_int32), P(C.c_double)]
+    L.pase_get_stats.argtypes = [ctx_p, P(pase_stats)]
+    L.pase_last_error.argtypes = [ctx_p]
+    L.pase_last_error.restype = C.c_char_p
+    L.pase_destroy.argtypes = [ctx_p]
+    L.pase_destroy.restype = None
+    L.pase_get_configs.argtypes = [ctx_p, P(C.c_int32), P(C.c_int32)]
+    L.pase_get_order.argtypes = [ctx_p, P(C.c_int32), P(C.c_int32), P(C.c_int32), P(C.c_int32)]
+    L.pase_get_cost_tables.argtypes = [ctx_p, C.c_int32, C.c_int32, P(C.c_double)]
+    L.pase_get_dp_table.argtypes = [ctx_p, C.c_int32, P(C.c_double), P(C.c_uint16)]
+    L.pase_table_entries.argtypes = [ctx_p, C.c_int32]
+    L.pase_table_entries.restype = C.c_int64
+    L.pase_set_cost_tables.argtypes = [ctx_p, P(C.c_double), P(C.c_double)]
+    L.pase_set_profiling.argtypes = [ctx_p, C.c_int32]
+    L.pase_get_unique_id.argtypes = [C.c_void_p]
+    for f in ("pase_create", "pase_solve", "pase_get_stats", "pase_get_configs", "pase_get_order",
+              "pase_get_cost_tables", "pase_get_dp_table", "pase_set_cost_tables", "pase_set_profiling",
+              "pase_get_unique_id"):
+        getattr(L, f).restype = C.c_int
+    _lib = L
+    return L
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+def marshal_graph(graph: dict):
+    """dict -> (pase_graph, keepalive).  Layout per include/pase.h."""
+    nodes = graph["nodes"]
+    edges = graph["edges"]
+    NA = (pase_node * max(len(nodes), 1))()
+    for v, nd in enumerate(nodes):
+        if nd["id"] != v:
+            raise ValueError(f"node {v}: id {nd['id']} must equal its index")
+        x = NA[v]
+        dims = nd["dims"]
+        if len(dims) > PASE_MAX_DIMS:
+            raise ValueError(f"node {v}: more than {PASE_MAX_DIMS} dims")
+        x.n_dims = len(dims)
+        for k, d in enumerate(dims):
+            x.size[k] = int(d["size"])
+            if d.get("splittable", True):
+                x.splittable_mask |= 1 << k
+        x.n_out_axes = len(nd["out_axes"])
+        for a, k in enumerate(nd["out_axes"]):
+            x.out_axes[a] = k
+        w = nd.get("w_axes") or []
+        x.n_w_axes = len(w)
+        for a, k in enumerate(w):
+            x.w_axes[a] = k
+        fd = nd.get("flop_dims")
+        x.flop_dims_mask = 0 if fd is None else sum(1 << k for k in fd)
+        x.flops_per_point = int(nd.get("flops_per_point", 2))
+        halo = nd.get("halo") or []
+        if len(halo) > PASE_MAX_HALO:
+            raise ValueError(f"node {v}: more than {PASE_MAX_HALO} halo pairs")
+        x.n_halo = len(halo)
+        for q, (h, f) in enumerate(halo):
+            x.halo_spatial[q], x.halo_filter[q] = h, f
+        x.elem_bytes = int(nd.get("elem_bytes", 4))
+    EA = (pase_edge * max(len(edges), 1))()
+    for e, ed in enumerate(edges):
+        EA[e].src, EA[e].dst = ed["src"], ed["dst"]
+        am = list(ed["axis_map"])
+        for a in range(PASE_MAX_DIMS):
+            EA[e].axis_map[a] = am[a] if a < len(am) else -1
+    g = pase_graph(len(nodes), NA, len(edges), EA)
+    return g, (NA, EA)
+
+
+def make_machine(flops: float = 1e13, bandwidth: float = 1e10, policy: int = PASE_CFG_EXACT_P,
+                 device: int = 0, stream: Optional[int] = None, rank: int = 0, world: int = 1,
+                 uid: Optional[bytes] = None, table_budget: int = 0,
+                 redundant_below: int = 4 << 20) -> pase_machine:
+    m = pase_machine()
+    m.flops_per_device, m.link_bandwidth = float(flops), float(bandwidth)
+    m.cfg_policy = int(policy)
+    m.table_budget_bytes = int(table_budget)
+    m.redundant_below_bytes = int(redundant_below)
+    m.cuda_device, m.rank, m.world = int(device), int(rank), int(world)
+    m._uid = C.create_string_buffer(uid, PASE_UID_BYTES) if uid else None
+    m.nccl_unique_id = C.cast(m._uid, C.c_void_p) if uid else None
+    m.cuda_stream = stream
+    return m
+
+
+class Context:
+    """Owns one pase_ctx (pase_create ... pase_destroy)."""
+
+    def __init__(self, graph: dict, p: int, policy="exact_p", flops: Optional[float] = None,
+                 bandwidth: Optional[float] = None, device: int = 0, stream: Optional[int] = None,
+                 rank: int = 0, world: int = 1, uid: Optional[bytes] = None, table_budget: int = 0,
+                 redundant_below: int = 4 << 20):
+        L = load()
+        mach_d = graph.get("machine") or {}
+        flops = flops if flops is not None else mach_d.get("flops", 1e13)
+        bandwidth = bandwidth if bandwidth is not None else mach_d.get("bandwidth", 1e10)
+        pol = POLICIES[policy] if isinstance(policy, str) else int(policy)
+        self.graph = graph
+        self.n, self.m = len(graph["nodes"]), len(graph["edges"])
+        g, self._keep = marshal_graph(graph)
+        self._mach = make_machine(flops, bandwidth, pol, device, stream, rank, world, uid, table_budget,
+                                  redundant_below)
+        h = C.c_void_p()
+        st = L.pase_create(C.byref(g), int(p), C.byref(self._mach), C.byref(h))
+        if st != 0:
+            raise PaseError(st, L.pase_last_error(None).decode())
+        self._h = h
+        self._L = L
+
+    def _chk(self, st: int) -> None:
+        if st != 0:
+            raise PaseError(st, self._L.pase_last_error(self._h).decode())
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._L.pase_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---- a5-a8
+    def solve(self) -> Dict[str, object]:
+        cfg = np.zeros((self.n, PASE_MAX_DIMS), np.int32)
+        idx = np.zeros(self.n, np.int32)
+        tot = C.c_double()
+        self._chk(self._L.pase_solve(self._h, _ptr(cfg, C.c_int32), _ptr(idx, C.c_int32), C.byref(tot)))
+        tuples = [tuple(int(c) for c in cfg[v, :len(self.graph["nodes"][v]["dims"])]) for v in range(self.n)]
+        return {"cost": tot.value, "config_index": idx, "configs": tuples}
+
+    def stats(self) -> Dict[str, float]:
+        s = pase_stats()
+        self._chk(self._L.pase_get_stats(self._h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in pase_stats._fields_}
+
+    # ---- introspection
+    def configs(self) -> List[np.ndarray]:
+        K = np.zeros(self.n, np.int32)
+        self._chk(self._L.pase_get_configs(self._h, _ptr(K, C.c_int32), None))
+        T = np.zeros((int(K.sum()), PASE_MAX_DIMS), np.int32)
+        self._chk(self._L.pase_get_configs(self._h, _ptr(K, C.c_int32), _ptr(T, C.c_int32)))
+        out, off = [], 0
+        for v in range(self.n):
+            d = len(self.graph["nodes"][v]["dims"])
+            out.append(T[off:off + K[v], :d].copy())
+            off += K[v]
+        return out
+
+    def K(self) -> np.ndarray:
+        K = np.zeros(self.n, np.int32)
+        self._chk(self._L.pase_get_configs(self._h, _ptr(K, C.c_int32), None))
+        return K
+
+    def order(self):
+        n = self.n
+        sigma = np.zeros(n, np.int32)
+        off = np.zeros(n + 1, np.int32)
+        ids = np.zeros(n * PASE_MAX_DEP + 1, np.int32)
+        par = np.zeros(n, np.int32)
+        self._chk(self._L.pase_get_order(self._h, _ptr(sigma, C.c_int32), _ptr(off, C.c_int32),
+                                         _ptr(ids, C.c_int32), _ptr(par, C.c_int32)))
+        return sigma, [ids[off[i]:off[i + 1]].tolist() for i in range(n)], par
+
+    def cost_tables(self):
+        K = self.K()
+        Ls = []
+        for v in range(self.n):
+            out = np.zeros(int(K[v]), np.float64)
+            self._chk(self._L.pase_get_cost_tables(self._h, v, 0, _ptr(out, C.c_double)))
+            Ls.append(out)
+        Ws = []
+        for e, ed in enumerate(self.graph["edges"]):
+            out = np.zeros((int(K[ed["src"]]), int(K[ed["dst"]])), np.float64)
+            self._chk(self._L.pase_get_cost_tables(self._h, e, 1, _ptr(out, C.c_double)))
+            Ws.append(out)
+        return Ls, Ws
+
+    def dp_table(self, rank: int):
+        n = self._L.pase_table_entries(self._h, rank)
+        T = np.zeros(n, np.float64)
+        A = np.zeros(n, np.uint16)
+        self._chk(self._L.pase_get_dp_table(self._h, rank, _ptr(T, C.c_double), _ptr(A, C.c_uint16)))
+        return T, A
+
+    def set_cost_tables(self, Ls: Sequence[np.ndarray], Ws: Sequence[np.ndarray]) -> None:
+        L = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float64).ravel() for x in Ls]))
+        W = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float64).ravel() for x in Ws])
+                                 if len(Ws) else np.zeros(1))
+        self._chk(self._L.pase_set_cost_tables(self._h, _ptr(L, C.c_double), _ptr(W, C.c_double)))
+
+
+def unique_id() -> bytes:
+    """pase_get_unique_id: NCCL unique id bytes for multi-GPU contexts (rank 0)."""
+    buf = C.create_string_buffer(PASE_UID_BYTES)
+    st = load().pase_get_unique_id(buf)
+    if st != 0:
+        raise PaseError(st, "pase_get_unique_id failed")
+    return buf.raw
+
+
+# C-ABI-named wrappers (same names as include/pase.h)
+def pase_create(graph: dict, p: int, **kw) -> Context:
+    return Context(graph, p, **kw)
+
+
+def pase_solve(ctx: Context) -> Dict[str, object]:
+    return ctx.solve()
+
+
+def pase_get_stats(ctx: Context) -> Dict[str, float]:
+    return ctx.stats()
+
+
+def pase_destroy(ctx: Context) -> None:
+    ctx.close()
+
+
+def solve(graph: dict, p: int, policy="exact_p", **kw) -> Dict[str, object]:
+    """One-shot search: create, solve, destroy.  Returns cost, configs, stats."""
+    with Context(graph, p, policy=policy, **kw) as ctx:
+        r = ctx.solve()
+        r["stats"] = ctx.stats()
+        return r

@@ -1,0 +1,144 @@
+"""C-ABI library checks that need no GPU: every symbol of include/pase.h is exported,
+the ctypes mirror matches the C struct layout, and the host core (rows a1-a4:
+ingest, C(v), SortNodes, elimination tree) agrees with the oracle on every graph.
+Uses host-only planning contexts (machine.cuda_device < 0): no device work."""
+import os
+import re
+import subprocess
+
+import ctypes as C
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2407_04001_b200 import build as B
+from paper_2407_04001_b200 import pase, zoo
+from tests.helpers import relabel
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "pase.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    B.build()
+    return pase.load()
+
+
+def declared_symbols():
+    txt = open(HDR).read()
+    return sorted(set(re.findall(r"^\s*(?:pase_status|const char\*|void|int64_t)\s+(pase_\w+)\s*\(", txt, re.M)))
+
+
+def test_exports_every_declared_symbol(lib):
+    syms = declared_symbols()
+    assert len(syms) >= 13
+    out = subprocess.run(["nm", "-D", "--defined-only", B.SO], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (pase_\w+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    assert set(pase.EXPORTS) == set(syms)
+    for s in syms:
+        getattr(lib, s)
+
+
+def test_struct_layout_matches_header(tmp_path):
+    probe = tmp_path / "probe.c"
+    probe.write_text("""
+#include <stdio.h>
+#include <stddef.h>
+#include "pase.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu\\n", sizeof(pase_node), sizeof(pase_edge), sizeof(pase_graph),
+         sizeof(pase_machine), sizeof(pase_stats));
+  printf("%zu %zu %zu %zu\\n", offsetof(pase_node, flops_per_point), offsetof(pase_node, elem_bytes),
+         offsetof(pase_machine, nccl_unique_id), offsetof(pase_stats, ms_create));
+  return 0;
+}
+""")
+    exe = tmp_path / "probe"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(probe), "-o", str(exe)])
+    lines = subprocess.check_output([str(exe)], text=True).split("\n")
+    sizes = [int(x) for x in lines[0].split()]
+    assert sizes == [C.sizeof(pase.pase_node), C.sizeof(pase.pase_edge), C.sizeof(pase.pase_graph),
+                     C.sizeof(pase.pase_machine), C.sizeof(pase.pase_stats)]
+    offs = [int(x) for x in lines[1].split()]
+    assert offs == [pase.pase_node.flops_per_point.offset, pase.pase_node.elem_bytes.offset,
+                    pase.pase_machine.nccl_unique_id.offset, pase.pase_stats.ms_create.offset]
+
+
+def check_plan_against_oracle(graph, p, policy):
+    ctx = pase.Context(graph, p, policy=policy, device=-1)
+    pol = pase.POLICIES[policy]
+    # a2: C(v) identical tuples, identical order
+    oc = O.configs(graph, p, pol)
+    gc = ctx.configs()
+    assert len(oc) == len(gc)
+    for a, b in zip(oc, gc):
+        assert np.array_equal(a, b)
+    # a3: sigma and D(i) identical (SortNodes readings C, D)
+    K = np.array([len(c) for c in oc], np.int32)
+    n = len(K)
+    P = O.Problem(graph, K, [np.zeros(k) for k in K],
+                  [np.zeros((K[e["src"]], K[e["dst"]])) for e in graph["edges"]])
+    osig, odeps = P.sortnodes()
+    sigma, deps, parent = ctx.order()
+    assert list(sigma) == list(osig)
+    assert deps == [list(map(int, d)) for d in odeps]
+    # a4: elimination tree == Fig. 5's connected subsets: S(i) lookups j are exactly children(i)
+    rank = {int(v): i for i, v in enumerate(sigma)}
+    for i in range(n):
+        s = P.sets(sigma, i)
+        js = sorted(max(rank[v] for v in comp) for comp in s["S"])
+        kids = [j for j in range(n) if parent[j] == i]
+        assert js == kids, (i, js, kids)
+    st = ctx.stats()
+    off, cand = P.table_sizes()
+    assert st["candidates"] == cand and st["table_entries"] == off[-1]
+    assert st["max_dep"] == max(len(d) for d in deps)
+    ctx.close()
+
+
+@pytest.mark.parametrize("name", ["mlp", "alexnet", "inception_v3", "rnnlm", "gnmt", "transformer"])
+def test_host_plan_matches_oracle_zoo(lib, name):
+    g, p = zoo.bench_graph(name)
+    check_plan_against_oracle(g, p, "exact_p")
+    if name in ("mlp", "alexnet", "transformer"):
+        check_plan_against_oracle(g, p, "le_p")
+
+
+def test_host_plan_matches_oracle_random(lib):
+    for seed in range(150):
+        g = zoo.random_model_graph(1 + seed % 11, seed, multi_p=0.2 if seed % 4 == 0 else 0.0)
+        check_plan_against_oracle(g, 4 << (seed % 3), "exact_p" if seed % 2 else "le_p")
+
+
+def test_host_plan_relabelled(lib):
+    g, p = zoo.bench_graph("inception_v3")
+    g2, _ = relabel(g, 3)
+    check_plan_against_oracle(g2, p, "exact_p")
+
+
+def test_invalid_inputs_fail_loudly(lib):
+    g = zoo.mlp()
+    g["edges"].append({"src": 0, "dst": 0, "axis_map": [0, 1]})
+    with pytest.raises(pase.PaseError) as ei:
+        pase.Context(g, 4, device=-1)
+    assert ei.value.status == 1 and "self-loop" in str(ei.value)
+    g = zoo.mlp()
+    g["edges"] = g["edges"][:1]                      # disconnected
+    with pytest.raises(pase.PaseError) as ei:
+        pase.Context(g, 4, device=-1)
+    assert ei.value.status == 1 and "connected" in str(ei.value)
+    g = zoo.mlp()
+    g["edges"][0]["axis_map"] = [0, 7]
+    with pytest.raises(pase.PaseError) as ei:
+        pase.Context(g, 4, device=-1)
+    assert ei.value.status == 1 and "edge 0" in str(ei.value)
+
+
+def test_solve_needs_device(lib):
+    ctx = pase.Context(zoo.mlp(), 4, device=-1)
+    with pytest.raises(pase.PaseError) as ei:
+        ctx.solve()
+    assert ei.value.status == 5
