@@ -39,6 +39,7 @@ WORKLOADS = {
     "rnnlm": ("rnnlm", 64, "exact_p", "RNNLM unrolled 2 layers x 40 steps, p=64, EXACT_P"),
     "alexnet": ("alexnet", 8, "exact_p", "AlexNet b128, p=8, EXACT_P"),
     "mlp": ("mlp", 4, "exact_p", "4-layer MLP b64 h256, p=4, EXACT_P"),
+    "chain200": ("chain200", 4, "exact_p", "latency probe: 200-GEMM path, p=4 (not a paper config)"),
 }
 SM_COUNT = 148
 FP64_LANES_PER_SM = 64          # B200 fp64 pipe, 37 TFLOP/s (FMA=2) / 148 SM / 1.965 GHz / 2

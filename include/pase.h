@@ -60,7 +60,7 @@ typedef enum { PASE_CFG_EXACT_P = 0, PASE_CFG_LE_P = 1 } pase_cfg_policy;
 /* One vertex = one layer with its iteration space. */
 typedef struct {
     int32_t n_dims;                        /* 1..PASE_MAX_DIMS */
-    int64_t size[PASE_MAX_DIMS];           /* extents, >= 1 */
+    int64_t size[PASE_MAX_DIMS];           /* extents, 1 <= size < 2^31 */
     uint32_t splittable_mask;              /* bit k: dim k may be split */
     int32_t n_out_axes;                    /* output tensor rank, 1..n_dims */
     int32_t out_axes[PASE_MAX_DIMS];       /* iteration dim of each output-tensor axis (distinct) */
@@ -170,6 +170,12 @@ int64_t pase_table_entries(const pase_ctx* ctx, int32_t rank);
  * over nodes in id order (K_v each), W over edges in id order (K_src*K_dst each, src-major).
  * Subsequent pase_solve calls use these tables instead of running the cost-table kernel. */
 pase_status pase_set_cost_tables(pase_ctx* ctx, const double* L, const double* W);
+
+/* Persistent-schedule timeline (tracing; enabled by env PASE_TRACE=1 at pase_create): per DP
+ * task of the last pase_solve, 4 int64 = {(smid << 32) | rank, t_claim_ns, t_start_ns, t_end_ns}
+ * (%globaltimer).  Copies min(cap, n_tasks) records into out (may be NULL); returns n_tasks
+ * (0 when tracing is off, -1 on a CUDA error). */
+int64_t pase_get_trace(const pase_ctx* ctx, int64_t* out, int64_t cap);
 
 /* Time the solve phases separately on the next pase_solve (adds syncs; default off). */
 pase_status pase_set_profiling(pase_ctx* ctx, int32_t enable);

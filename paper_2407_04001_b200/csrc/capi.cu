@@ -7,8 +7,10 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
+#include <queue>
 #include <string>
 #include <vector>
 
@@ -36,16 +38,25 @@ struct pase_ctx {
     int32_t* d_cfg = nullptr;
     int64_t* d_loff = nullptr;
     EdgeDesc* d_edges = nullptr;
-    int64_t* d_item_off = nullptr;
+    pase::CostChunk* d_chunks = nullptr;
+    int nchunks = 0;
     double* d_L = nullptr;
     double* d_W = nullptr;
     double* d_T = nullptr;
     uint16_t* d_A = nullptr;
     VertexDesc* d_vd = nullptr;
     TermDesc* d_td = nullptr;
-    int32_t* d_sigma = nullptr;
-    int32_t* d_dep_off = nullptr;
-    int32_t* d_dep_ids = nullptr;
+    pase::TaskDesc* d_tasks = nullptr;
+    int32_t* d_sched = nullptr;             // scheduler state (kernels.cu dp_persistent)
+    int32_t* d_order = nullptr;             // static task claim order
+    int32_t* d_sched_init = nullptr;        // its solve-start image (leaves queued)
+    size_t sched_bytes = 0;
+    int64_t* d_trace = nullptr;             // PASE_TRACE=1: 4 int64 per persistent task
+    int ntasks = 0, nblocks = 0;
+    bool persistent = true;
+    pase::BtDesc* d_bt = nullptr;
+    int32_t* d_bt_off = nullptr;
+    int nbtlev = 0;
     int32_t* d_choice = nullptr;
     double* d_total = nullptr;
     // host mirrors
@@ -53,9 +64,9 @@ struct pase_ctx {
     std::vector<TermDesc> td;
     int32_t* h_choice = nullptr;            // pinned
     double* h_total = nullptr;              // pinned
-    int64_t cost_total = 0;
     bool override_tables = false;
     bool solved = false;
+    bool no_graph = false;
     int profiling = 0;
     cudaGraphExec_t exec = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr, ev_dp = nullptr;
@@ -78,6 +89,41 @@ thread_local std::string g_create_err;
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Cost-table work list: edges first (row chunks of the later-endpoint configs), then vertices.
+std::vector<pase::CostChunk> cost_chunks(const Plan& P) {
+    std::vector<pase::CostChunk> ch;
+    for (int e = 0; e < P.m; ++e) {
+        const pase_edge& x = P.edges[e];
+        const int late = P.rank[x.src] > P.rank[x.dst] ? x.src : x.dst;
+        for (int r0 = 0; r0 < P.K[late]; r0 += pase::kCostRows)
+            ch.push_back({P.n + e, r0, std::min(pase::kCostRows, P.K[late] - r0), 0});
+    }
+    for (int v = 0; v < P.n; ++v) ch.push_back({v, 0, P.K[v], 0});
+    return ch;
+}
+int64_t nchunks_of(const Plan& P) { return (int64_t)cost_chunks(P).size(); }
+
+// Upper bound of persistent tasks (each vertex gets <= kTasksPerBlock * nblocks + 1 tasks).
+constexpr int kTasksPerBlock = 4;
+int64_t max_tasks_of(const Plan& P, int nblocks) {
+    int64_t t = 0;
+    for (int i = 0; i < P.n; ++i)
+        t += std::min<int64_t>(P.tsize[i], (int64_t)kTasksPerBlock * std::max(nblocks, 1) + 1);
+    return std::max<int64_t>(t, 1);
+}
+
+bool trace_on() {
+    const char* t = std::getenv("PASE_TRACE");
+    return t && t[0] == '1';
+}
+
+// lane-group size: each lane should own >= ~4 values of C (K=28 -> 4 lanes, K=205 -> 32)
+int lane_group_log2(int K) {
+    int g = 2;
+    while (g < 5 && (1 << (g + 1)) * 4 <= K) ++g;
+    return g;
+}
+
 // Carve all device buffers out of one allocation.
 pase_status allocate(pase_ctx* ctx) {
     const Plan& P = ctx->P;
@@ -96,16 +142,20 @@ pase_status allocate(pase_ctx* ctx) {
         {(void**)&ctx->d_cfg, sizeof(int32_t) * pase::kMaxDims * ncfg},
         {(void**)&ctx->d_loff, sizeof(int64_t) * (n + 1)},
         {(void**)&ctx->d_edges, sizeof(EdgeDesc) * std::max(m, 1)},
-        {(void**)&ctx->d_item_off, sizeof(int64_t) * (n + m + 1)},
+        {(void**)&ctx->d_chunks, sizeof(pase::CostChunk) * (size_t)nchunks_of(P)},
         {(void**)&ctx->d_L, sizeof(double) * P.loff[n]},
         {(void**)&ctx->d_W, sizeof(double) * std::max<int64_t>(P.woff[m], 1)},
         {(void**)&ctx->d_T, sizeof(double) * P.toff[n]},
         {(void**)&ctx->d_A, sizeof(uint16_t) * P.toff[n]},
         {(void**)&ctx->d_vd, sizeof(VertexDesc) * n},
         {(void**)&ctx->d_td, sizeof(TermDesc) * nterms_total},
-        {(void**)&ctx->d_sigma, sizeof(int32_t) * n},
-        {(void**)&ctx->d_dep_off, sizeof(int32_t) * (n + 1)},
-        {(void**)&ctx->d_dep_ids, sizeof(int32_t) * std::max<int64_t>((int64_t)n * pase::kMaxDep, 1)},
+        {(void**)&ctx->d_tasks, sizeof(pase::TaskDesc) * (size_t)max_tasks_of(P, ctx->nblocks)},
+        {(void**)&ctx->d_sched, sizeof(int32_t) * (pase::kSchedLine + (size_t)n)},
+        {(void**)&ctx->d_sched_init, sizeof(int32_t) * (pase::kSchedLine + (size_t)n)},
+        {(void**)&ctx->d_order, sizeof(int32_t) * (size_t)max_tasks_of(P, ctx->nblocks)},
+        {(void**)&ctx->d_trace, trace_on() ? sizeof(int64_t) * 4 * (size_t)max_tasks_of(P, ctx->nblocks) : 0},
+        {(void**)&ctx->d_bt, sizeof(pase::BtDesc) * n},
+        {(void**)&ctx->d_bt_off, sizeof(int32_t) * (n + 1)},
         {(void**)&ctx->d_choice, sizeof(int32_t) * n},
         {(void**)&ctx->d_total, sizeof(double)},
     };
@@ -145,15 +195,11 @@ pase_status upload(pase_ctx* ctx) {
         for (int a = 0; a < pase::kMaxDims; ++a) d.axis_map[a] = P.edges[e].axis_map[a];
         d.woff = P.woff[e];
     }
-    std::vector<int64_t> item_off(n + m + 1, 0);
-    for (int v = 0; v < n; ++v) item_off[v + 1] = item_off[v] + P.K[v];
-    for (int e = 0; e < m; ++e)
-        item_off[n + e + 1] = item_off[n + e] + (int64_t)P.K[P.edges[e].src] * P.K[P.edges[e].dst];
-    ctx->cost_total = item_off[n + m];
+    const std::vector<pase::CostChunk> chunks = cost_chunks(P);
+    ctx->nchunks = (int)chunks.size();
 
     ctx->vd.assign(n, VertexDesc{});
     ctx->td.clear();
-    std::vector<int32_t> dep_off(n + 1, 0), dep_ids;
     for (int i = 0; i < n; ++i) {
         const int v = P.sigma[i];
         VertexDesc& d = ctx->vd[i];
@@ -196,38 +242,176 @@ pase_status upload(pase_ctx* ctx) {
             ctx->td.push_back(tc);
         }
         d.nterms = (int32_t)ctx->td.size() - d.term0;
-        dep_off[i] = (int32_t)dep_ids.size();
-        dep_ids.insert(dep_ids.end(), P.dep[i].begin(), P.dep[i].end());
+        // tiled schedule: qstar = the coordinate whose first term is latest
+        // in the canonical order (longest hoistable prefix); ties -> larger radix, lower q.
+        {
+            const TermDesc* tv = ctx->td.data() + d.term0;
+            d.qstar = -1;
+            d.tstar = d.nterms;
+            int best_first = -1;
+            for (int q = 0; q < d.m; ++q) {
+                int first = -1;
+                for (int t = 0; t < d.nterms && first < 0; ++t)
+                    if (tv[t].stride[q] != 0) first = t;
+                if (first < 1) { ctx->err = "internal: D(i) coordinate not used by any term"; return PASE_ERR_STATE; }
+                if (first > best_first || (first == best_first && d.radix[q] > d.radix[d.qstar])) {
+                    best_first = first;
+                    d.qstar = q;
+                }
+            }
+            if (d.qstar >= 0) d.tstar = best_first;
+            d.rq = d.qstar >= 0 ? d.radix[d.qstar] : 1;
+            d.ntile = (d.rq + pase::kTile - 1) / pase::kTile;
+            d.ostride_q = 1;
+            for (int q = 0; q < d.qstar; ++q) d.ostride_q *= d.radix[q];
+            if (d.qstar < 0) d.ostride_q = 0;
+            d.ncombo = d.nout / d.rq;
+            d.nitems = d.ncombo * d.ntile;
+            bool wide = d.nitems >= (int64_t(1) << 31);              // 32-bit item decode
+            for (int t = 0; t < d.nterms; ++t)
+                for (int q = 0; q < d.m; ++q)
+                    if (tv[t].stride[q] >= (int64_t(1) << 31) / 16) wide = true;
+            const int NP = d.tstar, NS = d.nterms - d.tstar;
+            if (!wide && NP >= 1 && NP <= 4 && NS >= 0 && NS <= 3) {
+                d.glog = lane_group_log2(d.K);
+                d.shape = (NP - 1) * 16 + NS * 4 + (d.glog - 2);
+            } else {                                                 // generic kernel
+                d.glog = d.K <= 4 ? 2 : d.K <= 8 ? 3 : d.K <= 16 ? 4 : 5;
+                d.shape = -1;
+            }
+            // persistent tasks: one item per lane group of a CTA for small vertices (latency),
+            // about kTasksPerBlock tasks per CTA of the grid for the big ones (balance)
+            const int64_t units = d.shape >= 0 ? d.nitems : d.nout;
+            const int64_t groups = 256 >> d.glog;
+            const int64_t spread = (int64_t)kTasksPerBlock * std::max(ctx->nblocks, 1);
+            int64_t ti = std::max<int64_t>(groups, (units + spread - 1) / spread);
+            ti = (ti + groups - 1) / groups * groups;
+            d.ntasks = (int32_t)((units + ti - 1) / ti);
+            d.items_per_task = (int32_t)std::min<int64_t>(ti, INT32_MAX);
+            d.parent = P.parent[i];
+        }
     }
-    dep_off[n] = (int32_t)dep_ids.size();
-    if (dep_ids.empty()) dep_ids.push_back(0);
+    // persistent schedule: tasks in rank order (a topological order of the tree)
+    std::vector<pase::TaskDesc> tasks;
+    for (int i = 0; i < n; ++i) {
+        VertexDesc& d = ctx->vd[i];
+        const int64_t units = d.shape >= 0 ? d.nitems : d.nout, ti = d.items_per_task;
+        d.task0 = (int32_t)tasks.size();
+        for (int64_t a = 0; a < units; a += ti) tasks.push_back({i, 0, a, std::min(units, a + ti)});
+        if ((int64_t)tasks.size() - d.task0 != d.ntasks) { ctx->err = "internal: task count"; return PASE_ERR_STATE; }
+    }
+    if ((int64_t)tasks.size() > max_tasks_of(P, ctx->nblocks)) { ctx->err = "internal: task bound"; return PASE_ERR_STATE; }
+    ctx->ntasks = (int)tasks.size();
+    // Static claim order: list-schedule the task DAG on nblocks simulated CTAs, ready tasks
+    // by decreasing bottom level (longest estimated path to the root), i.e. critical path
+    // first.  Estimated task time: ~3 us of dependent-latency overhead + candidates at
+    // ~3e9 candidates/s per CTA.
+    const int64_t ntk = (int64_t)tasks.size();
+    std::vector<double> tdur(ntk), bl(n, 0.0);
+    for (int64_t t = 0; t < ntk; ++t) {
+        const VertexDesc& d = ctx->vd[tasks[t].vtx];
+        const double cand = (double)(tasks[t].i1 - tasks[t].i0) * d.K * (d.shape >= 0 ? pase::kTile : 1);
+        tdur[t] = 3.0 + cand / 3000.0;
+    }
+    for (int i = n - 1; i >= 0; --i) {              // parents have higher ranks
+        const VertexDesc& d = ctx->vd[i];
+        const double vt = std::max(tdur[d.task0], (double)d.ntasks * tdur[d.task0] / std::max(ctx->nblocks, 1));
+        bl[i] = vt + (P.parent[i] >= 0 ? bl[P.parent[i]] : 0.0);
+    }
+    std::vector<int32_t> order;
+    order.reserve(ntk);
+    {
+        std::vector<int64_t> pend(n, 0);
+        for (int i = 0; i < n; ++i)
+            for (int j : P.children[i]) pend[i] += ctx->vd[j].ntasks;
+        using RT = std::pair<double, int32_t>;                         // (priority, -task)
+        std::priority_queue<RT> ready;
+        using EV = std::pair<double, int32_t>;                         // (finish time, task)
+        std::priority_queue<EV, std::vector<EV>, std::greater<EV>> events;
+        auto release = [&](int v) {
+            for (int k = 0; k < ctx->vd[v].ntasks; ++k) ready.push({bl[v], -(ctx->vd[v].task0 + k)});
+        };
+        for (int i = 0; i < n; ++i)
+            if (P.children[i].empty()) release(i);
+        int free_w = std::max(ctx->nblocks, 1);
+        double now = 0.0;
+        while ((int64_t)order.size() < ntk) {
+            while (free_w > 0 && !ready.empty()) {
+                const int32_t t = -ready.top().second;
+                ready.pop();
+                order.push_back(t);
+                --free_w;
+                events.push({now + tdur[t], t});
+            }
+            if (events.empty()) { ctx->err = "internal: task DAG is not schedulable"; return PASE_ERR_STATE; }
+            const EV e = events.top();
+            events.pop();
+            now = e.first;
+            ++free_w;
+            const int par = P.parent[tasks[e.second].vtx];
+            if (par >= 0 && --pend[par] == 0) release(par);
+        }
+    }
+    // scheduler state at solve start: [claim counter | pending[n]]
+    std::vector<int32_t> sched(pase::kSchedLine + (size_t)n, 0);
+    for (int i = 0; i < n; ++i)
+        for (int j : P.children[i]) sched[pase::kSchedLine + i] += ctx->vd[j].ntasks;
+    ctx->sched_bytes = sizeof(int32_t) * sched.size();
+    // back-substitution levels: lev(root) = 0, lev(i) = 1 + max lev over D(i)
+    std::vector<int> blev(n, 0);
+    int nlev = 0;
+    for (int i = n - 1; i >= 0; --i) {
+        int l = 0;
+        for (int u : P.dep[i]) l = std::max(l, blev[P.rank[u]] + 1);
+        blev[i] = l;
+        nlev = std::max(nlev, l + 1);
+    }
+    std::vector<int32_t> bt_off(nlev + 1, 0);
+    for (int i = 0; i < n; ++i) bt_off[blev[i] + 1]++;
+    for (int l = 0; l < nlev; ++l) bt_off[l + 1] += bt_off[l];
+    std::vector<pase::BtDesc> bt(n);
+    {
+        std::vector<int32_t> fill(bt_off.begin(), bt_off.end() - 1);
+        for (int i = n - 1; i >= 0; --i) {
+            pase::BtDesc& b = bt[fill[blev[i]]++];
+            b = pase::BtDesc{};
+            b.A = ctx->vd[i].A;
+            b.node = P.sigma[i];
+            b.m = (int32_t)P.dep[i].size();
+            for (int a = 0; a < b.m; ++a) { b.dep[a] = P.dep[i][a]; b.radix[a] = P.K[P.dep[i][a]]; }
+        }
+    }
+    ctx->nbtlev = nlev;
     cudaStream_t s = ctx->stream;
     ctx->h2d_bytes = sizeof(pase_node) * n + sizeof(int32_t) * n + sizeof(int64_t) * (n + 1) * 2 +
                      sizeof(int32_t) * P.cfg.size() + sizeof(EdgeDesc) * ed.size() +
-                     sizeof(int64_t) * (n + m + 1) + sizeof(VertexDesc) * n + sizeof(TermDesc) * ctx->td.size() +
-                     sizeof(int32_t) * (2 * n + 1 + dep_ids.size());
+                     sizeof(pase::CostChunk) * chunks.size() + sizeof(VertexDesc) * n + sizeof(TermDesc) * ctx->td.size() +
+                     sizeof(pase::BtDesc) * n + sizeof(int32_t) * (nlev + 1) +
+                     sizeof(pase::TaskDesc) * tasks.size() + ctx->sched_bytes + sizeof(int32_t) * order.size();
     CUDA_TRY(cudaMemcpyAsync(ctx->d_nodes, P.nodes.data(), sizeof(pase_node) * n, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_K, P.K.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_cfg_off, P.cfg_off.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_cfg, P.cfg.data(), sizeof(int32_t) * P.cfg.size(), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_loff, P.loff.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_edges, ed.data(), sizeof(EdgeDesc) * ed.size(), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_item_off, item_off.data(), sizeof(int64_t) * (n + m + 1), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_chunks, chunks.data(), sizeof(pase::CostChunk) * chunks.size(), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_vd, ctx->vd.data(), sizeof(VertexDesc) * n, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_td, ctx->td.data(), sizeof(TermDesc) * ctx->td.size(), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_sigma, P.sigma.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_dep_off, dep_off.data(), sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_dep_ids, dep_ids.data(), sizeof(int32_t) * dep_ids.size(), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_tasks, tasks.data(), sizeof(pase::TaskDesc) * tasks.size(), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_sched_init, sched.data(), ctx->sched_bytes, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_order, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_bt, bt.data(), sizeof(pase::BtDesc) * n, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_bt_off, bt_off.data(), sizeof(int32_t) * (nlev + 1), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaStreamSynchronize(s));   // host vectors above are stack-local
     return PASE_OK;
 }
 
 // Record the whole solve as one CUDA graph.  DP kernels are issued in rank order; a vertex
 // waits on its children's events only, so independent subtrees overlap.
-pase_status record_graph(pase_ctx* ctx) {
+pase_status issue_schedule(pase_ctx* ctx, bool capture) {
     const Plan& P = ctx->P;
     const int n = P.n;
-    if (ctx->exec) { cudaGraphExecDestroy(ctx->exec); ctx->exec = nullptr; }
+    if (capture && ctx->exec) { cudaGraphExecDestroy(ctx->exec); ctx->exec = nullptr; }
     const int nstreams = 4;
     if (ctx->aux.empty()) {
         ctx->aux.resize(nstreams);
@@ -240,15 +424,22 @@ pase_status record_graph(pase_ctx* ctx) {
     std::vector<cudaEvent_t> join(nstreams);
     for (auto& e : join) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     cudaStream_t s = ctx->stream;
-    CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    if (capture) CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    const unsigned ext = capture ? cudaEventRecordExternal : cudaEventRecordDefault;
     if (!ctx->override_tables)
         pase::launch_cost_tables(ctx->d_nodes, ctx->d_K, ctx->d_cfg_off, ctx->d_cfg, ctx->d_loff, n,
-                                 ctx->d_edges, P.m, ctx->d_item_off, ctx->cost_total, P.r, ctx->d_L,
+                                 ctx->d_edges, ctx->d_chunks, ctx->nchunks, P.r, ctx->d_L,
                                  ctx->d_W, s);
     // phase split: external event nodes (plain records would only become capture edges)
-    CUDA_TRY(cudaEventRecordWithFlags(ctx->ev_mid, s, cudaEventRecordExternal));
-    CUDA_TRY(cudaEventRecord(start, s));
+    CUDA_TRY(cudaEventRecordWithFlags(ctx->ev_mid, s, ext));
     std::vector<char> used(nstreams, 0);
+    if (ctx->persistent) {
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_sched, ctx->d_sched_init, ctx->sched_bytes, cudaMemcpyDeviceToDevice, s));
+        pase::launch_dp_persistent(ctx->d_vd, ctx->d_td, ctx->d_tasks, ctx->d_order, ctx->ntasks, ctx->d_sched,
+                                   ctx->nblocks,
+                                   trace_on() ? ctx->d_trace : nullptr, s);
+    } else {
+    CUDA_TRY(cudaEventRecord(start, s));
     // assign each vertex the stream of its first child (chains stay on one stream)
     std::vector<int> sid(n, -1);
     int rr = 0;
@@ -266,22 +457,35 @@ pase_status record_graph(pase_ctx* ctx) {
             CUDA_TRY(cudaEventRecord(join[k], ctx->aux[k]));
             CUDA_TRY(cudaStreamWaitEvent(s, join[k], 0));
         }
-    CUDA_TRY(cudaEventRecordWithFlags(ctx->ev_dp, s, cudaEventRecordExternal));
-    pase::launch_backtrack(ctx->d_sigma, ctx->d_dep_off, ctx->d_dep_ids, ctx->d_vd, n, ctx->d_choice,
+    }
+    CUDA_TRY(cudaEventRecordWithFlags(ctx->ev_dp, s, ext));
+    pase::launch_backtrack(ctx->d_bt, ctx->d_bt_off, ctx->nbtlev, n, ctx->vd[n - 1].T, ctx->d_choice,
                            ctx->d_total, s);
     CUDA_TRY(cudaMemcpyAsync(ctx->h_choice, ctx->d_choice, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->h_total, ctx->d_total, sizeof(double), cudaMemcpyDeviceToHost, s));
-    cudaGraph_t graph;
-    cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    cudaError_t ce = cudaSuccess;
+    cudaGraph_t graph = nullptr;
+    if (capture) ce = cudaStreamEndCapture(s, &graph);
     for (auto& e : done) cudaEventDestroy(e);
     for (auto& e : join) cudaEventDestroy(e);
     cudaEventDestroy(start);
     if (ce != cudaSuccess) { ctx->err = std::string("stream capture: ") + cudaGetErrorString(ce); return PASE_ERR_CUDA; }
-    ce = cudaGraphInstantiate(&ctx->exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (ce != cudaSuccess) { ctx->err = std::string("graph instantiate: ") + cudaGetErrorString(ce); return PASE_ERR_CUDA; }
-    ctx->stats.n_launches = (ctx->override_tables ? 0 : 1) + n + 1;
+    if (capture) {
+        ce = cudaGraphInstantiate(&ctx->exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) { ctx->err = std::string("graph instantiate: ") + cudaGetErrorString(ce); return PASE_ERR_CUDA; }
+    }
     return PASE_OK;
+}
+
+// The solve schedule is recorded once as a CUDA graph; PASE_NO_GRAPH=1 issues it directly
+// on the streams at every solve instead (profiling: kernels then launch in rank order).
+pase_status record_graph(pase_ctx* ctx) {
+    ctx->stats.n_launches = (ctx->override_tables ? 0 : 1) + (ctx->persistent ? 1 : ctx->P.n) + 1;
+    const char* ng = std::getenv("PASE_NO_GRAPH");
+    ctx->no_graph = ng && ng[0] == '1';
+    if (ctx->no_graph) return PASE_OK;
+    return issue_schedule(ctx, true);
 }
 
 void fill_stats(pase_ctx* ctx) {
@@ -371,22 +575,45 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
         ctx->err = "cudaEventCreate failed";
         return fail(PASE_ERR_CUDA);
     }
+    {
+        const char* sc = std::getenv("PASE_SCHEDULE");
+        ctx->persistent = !(sc && std::strcmp(sc, "launches") == 0);
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev) != cudaSuccess || sms < 1) {
+            ctx->err = "cudaDeviceGetAttribute(MultiProcessorCount) failed";
+            return fail(PASE_ERR_CUDA);
+        }
+        ctx->nblocks = std::max(1, pase::persistent_blocks_per_sm()) * sms;
+    }
+    auto t_plan = std::chrono::steady_clock::now();
     if ((st = allocate(ctx))) return fail(st);
+    auto t_alloc = std::chrono::steady_clock::now();
     if ((st = upload(ctx))) return fail(st);
+    auto t_upload = std::chrono::steady_clock::now();
     if ((st = record_graph(ctx))) return fail(st);
+    auto t_graph = std::chrono::steady_clock::now();
     fill_stats(ctx);
-    ctx->stats.ms_create =
-        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    using ms = std::chrono::duration<double, std::milli>;
+    ctx->stats.ms_create = ms(t_graph - t0).count();
+    if (const char* tv = std::getenv("PASE_TIMING"); tv && tv[0] == '1')
+        std::fprintf(stderr, "[pase] create: plan+setup %.3f ms, alloc %.3f ms, upload %.3f ms, graph %.3f ms\n",
+                     ms(t_plan - t0).count(), ms(t_alloc - t_plan).count(), ms(t_upload - t_alloc).count(),
+                     ms(t_graph - t_upload).count());
     *out = ctx;
     return PASE_OK;
 }
 
 pase_status pase_solve(pase_ctx* ctx, int32_t* configs_out, int32_t* config_index_out, double* total_cost_out) {
     if (!ctx) return PASE_ERR_INVALID;
-    if (!ctx->exec) { ctx->err = "context has no solve schedule (host-only planning context?)"; return PASE_ERR_STATE; }
+    if (!ctx->exec && !ctx->no_graph) { ctx->err = "context has no solve schedule (host-only planning context?)"; return PASE_ERR_STATE; }
     CUDA_TRY(cudaSetDevice(ctx->dev));
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
-    CUDA_TRY(cudaGraphLaunch(ctx->exec, ctx->stream));
+    if (ctx->no_graph) {
+        pase_status st = issue_schedule(ctx, false);
+        if (st) return st;
+    } else {
+        CUDA_TRY(cudaGraphLaunch(ctx->exec, ctx->stream));
+    }
     CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     float ms = 0.f;
@@ -528,6 +755,15 @@ pase_status pase_set_cost_tables(pase_ctx* ctx, const double* L, const double* W
         if (st) return st;
     }
     return PASE_OK;
+}
+
+int64_t pase_get_trace(const pase_ctx* ctx_c, int64_t* out, int64_t cap) {
+    pase_ctx* ctx = const_cast<pase_ctx*>(ctx_c);
+    if (!ctx || ctx->dev < 0 || !ctx->d_trace || !trace_on()) return 0;
+    const int64_t nt = std::min<int64_t>(ctx->ntasks, cap);
+    if (out && nt > 0 && cudaMemcpy(out, ctx->d_trace, sizeof(int64_t) * 4 * nt, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
+    return ctx->ntasks;
 }
 
 pase_status pase_set_profiling(pase_ctx* ctx, int32_t enable) {

@@ -28,7 +28,10 @@ pase_status validate(const pase_graph* g, std::string& err) {
         const pase_node& x = g->nodes[v];
         if (x.n_dims < 1 || x.n_dims > kMaxDims) { err = fmt("node %lld: n_dims %lld out of range", v, x.n_dims); return PASE_ERR_INVALID; }
         for (int k = 0; k < x.n_dims; ++k)
-            if (x.size[k] < 1) { err = fmt("node %lld: dim %lld has size < 1", v, k); return PASE_ERR_INVALID; }
+            if (x.size[k] < 1 || x.size[k] > 0x7fffffff) {
+                err = fmt("node %lld: dim %lld size out of range [1, 2^31)", v, k);
+                return PASE_ERR_INVALID;
+            }
         if (x.n_out_axes < 1 || x.n_out_axes > x.n_dims) { err = fmt("node %lld: bad n_out_axes", v); return PASE_ERR_INVALID; }
         if (x.n_w_axes < 0 || x.n_w_axes > x.n_dims) { err = fmt("node %lld: bad n_w_axes", v); return PASE_ERR_INVALID; }
         uint32_t seen = 0;
@@ -82,31 +85,55 @@ void splits_of(const pase_node& x, int k, int p, std::vector<int>& out) {
         if (p % c == 0 && x.size[k] % c == 0) out.push_back(c);
 }
 
-// Lexicographic product (dim 0 most significant) filtered by the policy.
-void enumerate(const pase_node& x, int p, int policy, std::vector<int32_t>& rows) {
-    std::vector<std::vector<int>> opt(x.n_dims);
-    for (int k = 0; k < x.n_dims; ++k) splits_of(x, k, p, opt[k]);
-    // recursive product with running value
-    std::vector<std::vector<int32_t>> all;
-    std::vector<int32_t> cur(kMaxDims, 1);
+// Lexicographic product (dim 0 most significant) filtered by the policy.  Depth-first over
+// the ascending split lists, pruned by the running product; no per-tuple allocation.
+struct Enum {
+    int nd, p;
+    int opt[kMaxDims][64], nopt[kMaxDims];
+    int32_t cur[kMaxDims];
+    std::vector<int32_t>* rows;
     std::vector<int64_t> prods;
-    auto rec = [&](auto&& self, int k, int64_t prod) -> void {
-        if (k == x.n_dims) { all.push_back(cur); prods.push_back(prod); return; }
-        for (int c : opt[k]) {
-            if (prod * c > p) break;           // ascending splits: larger ones exceed p too
+    void rec(int k, int64_t prod) {
+        if (k == nd) {
+            rows->insert(rows->end(), cur, cur + kMaxDims);
+            prods.push_back(prod);
+            return;
+        }
+        for (int i = 0; i < nopt[k]; ++i) {
+            const int c = opt[k][i];
+            if (prod * c > p) break;          // ascending: larger splits exceed p too
             cur[k] = c;
-            self(self, k + 1, prod * c);
+            rec(k + 1, prod * c);
         }
         cur[k] = 1;
-    };
-    rec(rec, 0, 1);
-    int64_t target = 0;
-    if (policy == PASE_CFG_EXACT_P)
-        for (int64_t q : prods) target = std::max(target, q);
+    }
+};
+
+void enumerate(const pase_node& x, int p, int policy, std::vector<int32_t>& rows) {
+    Enum E;
+    E.nd = x.n_dims;
+    E.p = p;
+    std::vector<int> tmp;
+    for (int k = 0; k < x.n_dims; ++k) {
+        splits_of(x, k, p, tmp);
+        E.nopt[k] = (int)tmp.size();
+        for (int i = 0; i < E.nopt[k]; ++i) E.opt[k][i] = tmp[i];
+    }
+    for (int k = 0; k < kMaxDims; ++k) E.cur[k] = 1;
     rows.clear();
-    for (size_t i = 0; i < all.size(); ++i)
-        if (policy == PASE_CFG_LE_P || prods[i] == target)
-            rows.insert(rows.end(), all[i].begin(), all[i].end());
+    E.rows = &rows;
+    E.rec(0, 1);
+    if (policy == PASE_CFG_EXACT_P) {         // keep the tuples of the largest product <= p
+        int64_t target = 0;
+        for (int64_t q : E.prods) target = std::max(target, q);
+        size_t w = 0;
+        for (size_t i = 0; i < E.prods.size(); ++i)
+            if (E.prods[i] == target) {
+                if (w != i) std::copy(rows.begin() + i * kMaxDims, rows.begin() + (i + 1) * kMaxDims, rows.begin() + w * kMaxDims);
+                ++w;
+            }
+        rows.resize(w * kMaxDims);
+    }
 }
 
 // ---------------------------------------------------------------- a3
@@ -261,10 +288,11 @@ pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* mach,
             return PASE_ERR_RESOURCE;
         }
         P.tsize[i] = s;
-        P.toff[i + 1] = P.toff[i] + s;
+        P.toff[i + 1] = P.toff[i] + (s + 15) / 16 * 16;   // 128-B aligned tables (no shared L1 lines)
         P.candidates += (uint64_t)s * (uint64_t)P.K[P.sigma[i]];
     }
-    P.entries = (uint64_t)P.toff[n];
+    P.entries = 0;
+    for (int i = 0; i < n; ++i) P.entries += (uint64_t)P.tsize[i];
     P.loff.assign(n + 1, 0);
     for (int v = 0; v < n; ++v) P.loff[v + 1] = P.loff[v] + P.K[v];
     P.woff.assign(m + 1, 0);

@@ -58,136 +58,244 @@ __device__ double d_layer_cost(const pase_node& x, const int32_t* c, double r) {
     return __dadd_rn(__ull2double_rn((unsigned long long)compute), __dmul_rn(r, comm));
 }
 
-// t_x bytes (DESIGN reading K): nested aligned layouts; per output axis of the producer
-// held = ext / c_src, need = ceil(ext / c_dst[map]) (ext if unmapped), overlap = min.
-__device__ int64_t d_transfer_bytes(const pase_node& u, const int32_t* cu, const int32_t* cv,
-                                    const int32_t* amap) {
-    int64_t need = 1, ov = 1;
-    for (int a = 0; a < u.n_out_axes; ++a) {
-        const int du = u.out_axes[a];
-        const int64_t ext = u.size[du];
-        const int64_t held = ext / cu[du];
-        const int64_t nd = amap[a] < 0 ? ext : (ext + cv[amap[a]] - 1) / cv[amap[a]];
-        need *= nd;
-        ov *= nd < held ? nd : held;
-    }
-    return 2 * (int64_t)u.elem_bytes * (need - ov);
-}
+// One CTA per chunk: a vertex (all K_v entries of L_v) or up to kCostRows rows of one
+// edge table W_e[row = later endpoint config][col = earlier endpoint config].  Per-config,
+// per-axis shard extents (and prod need) are precomputed in shared memory, so the inner
+// loop is a min / multiply per axis, and stores are coalesced along the column.
+constexpr int kCostCols = 512;
 
 __global__ void __launch_bounds__(256)
 cost_tables_kernel(const pase_node* __restrict__ nodes, const int32_t* __restrict__ K,
                    const int64_t* __restrict__ cfg_off, const int32_t* __restrict__ cfg,
-                   const int64_t* __restrict__ loff, int n, const EdgeDesc* __restrict__ edges, int m,
-                   const int64_t* __restrict__ item_off, int64_t total, double r,
-                   double* __restrict__ L, double* __restrict__ W) {
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        int lo = 0, hi = n + m;                       // item_off[lo] <= idx < item_off[hi]
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (item_off[mid] <= idx) lo = mid; else hi = mid;
+                   const int64_t* __restrict__ loff, int n, const EdgeDesc* __restrict__ edges,
+                   const CostChunk* __restrict__ chunks, double r, double* __restrict__ L,
+                   double* __restrict__ W) {
+    // [axis][config] layouts: lanes of a warp read consecutive configs (conflict-free)
+    __shared__ uint32_t rowq[kMaxDims][kCostRows];
+    __shared__ uint32_t colq[kMaxDims][kCostCols];
+    __shared__ uint64_t rowprod[kCostRows];
+    __shared__ uint64_t colprod[kCostCols];
+    const CostChunk ch = chunks[blockIdx.x];
+    if (ch.item < n) {
+        const int v = ch.item;
+        for (int c = threadIdx.x; c < K[v]; c += blockDim.x)
+            L[loff[v] + c] = d_layer_cost(nodes[v], cfg + (cfg_off[v] + c) * kMaxDims, r);
+        return;
+    }
+    const EdgeDesc& e = edges[ch.item - n];
+    const pase_node& u = nodes[e.src];
+    const int nax = u.n_out_axes;
+    const int early = e.later_is_src ? e.dst : e.src;
+    const int Ke = K[early];
+    const uint64_t elem2 = 2ull * (uint64_t)u.elem_bytes;
+    // t_x (DESIGN reading K): per output axis a of src, held_a = ext / c_src, need_a =
+    // ceil(ext / c_dst[map_a]) (ext if unmapped); t_x = 2 elem (prod need - prod min(need, held))
+    auto held = [&](int cs, int a) -> uint32_t {
+        const int32_t* c = cfg + (cfg_off[e.src] + cs) * kMaxDims;
+        return (uint32_t)(u.size[u.out_axes[a]] / c[u.out_axes[a]]);
+    };
+    auto need = [&](int cd, int a) -> uint32_t {
+        const int32_t* c = cfg + (cfg_off[e.dst] + cd) * kMaxDims;
+        const int64_t ext = u.size[u.out_axes[a]];
+        return (uint32_t)(e.axis_map[a] < 0 ? ext : (ext + c[e.axis_map[a]] - 1) / c[e.axis_map[a]]);
+    };
+    // rows = later endpoint: src configs (held) if later_is_src, else dst configs (need)
+    for (int rr = threadIdx.x; rr < ch.nrows; rr += blockDim.x) {
+        uint64_t pr = 1;
+        for (int a = 0; a < nax; ++a) {
+            const uint32_t x = e.later_is_src ? held(ch.row0 + rr, a) : need(ch.row0 + rr, a);
+            rowq[a][rr] = x;
+            pr *= x;
         }
-        const int64_t local = idx - item_off[lo];
-        if (lo < n) {
-            const int v = lo;
-            L[loff[v] + local] = d_layer_cost(nodes[v], cfg + (cfg_off[v] + local) * kMaxDims, r);
-        } else {
-            const EdgeDesc& e = edges[lo - n];
-            // W_e row = config of the later-ranked endpoint, column = earlier endpoint (stride 1)
-            const int early = e.later_is_src ? e.dst : e.src;
-            const int64_t row = local / K[early], col = local % K[early];
-            const int64_t cs = e.later_is_src ? row : col, cd = e.later_is_src ? col : row;
-            const int64_t b = d_transfer_bytes(nodes[e.src], cfg + (cfg_off[e.src] + cs) * kMaxDims,
-                                               cfg + (cfg_off[e.dst] + cd) * kMaxDims, e.axis_map);
-            W[e.woff + local] = __dmul_rn(r, __ull2double_rn((unsigned long long)b));
+        rowprod[rr] = pr;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int c0 = 0; c0 < Ke; c0 += kCostCols) {
+        const int nc = min(kCostCols, Ke - c0);
+        __syncthreads();
+        for (int cc = threadIdx.x; cc < nc; cc += blockDim.x) {
+            uint64_t pr = 1;
+            for (int a = 0; a < nax; ++a) {
+                const uint32_t x = e.later_is_src ? need(c0 + cc, a) : held(c0 + cc, a);
+                colq[a][cc] = x;
+                pr *= x;
+            }
+            colprod[cc] = pr;
+        }
+        __syncthreads();
+        for (int rr = warp; rr < ch.nrows; rr += nw) {
+            double* out = W + e.woff + (int64_t)(ch.row0 + rr) * Ke + c0;
+            for (int cc = lane; cc < nc; cc += 32) {
+                uint64_t ov = 1;
+                for (int a = 0; a < nax; ++a) ov *= (uint64_t)min(rowq[a][rr], colq[a][cc]);
+                const uint64_t nd = e.later_is_src ? colprod[cc] : rowprod[rr];
+                out[cc] = __dmul_rn(r, __ull2double_rn((unsigned long long)(elem2 * (nd - ov))));
+            }
         }
     }
 }
 
 void launch_cost_tables(const pase_node* nodes_dev, const int32_t* K_dev, const int64_t* cfg_off_dev,
                         const int32_t* cfg_dev, const int64_t* loff_dev, int n,
-                        const EdgeDesc* edges_dev, int m, const int64_t* item_off_dev,
-                        int64_t total, double r, double* L_dev, double* W_dev, void* stream) {
-    const int threads = 256;
-    int64_t blocks = (total + threads - 1) / threads;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    if (blocks < 1) blocks = 1;
-    cost_tables_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
-        nodes_dev, K_dev, cfg_off_dev, cfg_dev, loff_dev, n, edges_dev, m, item_off_dev, total, r,
-        L_dev, W_dev);
+                        const EdgeDesc* edges_dev, const CostChunk* chunks_dev, int nchunks,
+                        double r, double* L_dev, double* W_dev, void* stream) {
+    cost_tables_kernel<<<(unsigned)nchunks, 256, 0, (cudaStream_t)stream>>>(
+        nodes_dev, K_dev, cfg_off_dev, cfg_dev, loff_dev, n, edges_dev, chunks_dev, r, L_dev, W_dev);
 }
 
 // =====================================================================================
-// K2: DP fill, v1 (generic): a lane group of g = pow2 >= min(K, 32) lanes per output phi.
+// K2: DP fill, tiled.
+//   Work item = one combination of the D(i) coordinates other than qstar, times a tile of
+//   up to kTile consecutive values of qstar.  A lane group of G lanes splits the reduction
+//   over C (lane l takes C = l, l+G, ...; loads of every table row are coalesced over C).
+//   Per C the prefix of the canonical sum over terms [0, tstar) -- which do not depend on
+//   qstar -- is computed once and reused by the kTile outputs of the tile (loop-invariant
+//   hoisting of a prefix only: the association ((L + W..) + T..) is unchanged, so results
+//   stay bit-identical to the oracle).  The (cost, C) pairs are then reduced across the
+//   group with a butterfly reduce-scatter (each exchange halves the values a lane holds).
+//   Table reads use ld.global.ca (not the non-coherent path): in the persistent schedule a
+//   child table is written earlier in the same kernel.
 // =====================================================================================
-template <int NT>
-__global__ void __launch_bounds__(256)
-dp_fill_kernel(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ tds, int vtx, int glog) {
-    __shared__ VertexDesc vd;
-    __shared__ TermDesc td[NT];
-    if (threadIdx.x == 0) vd = vds[vtx];
-    for (int t = threadIdx.x; t < NT; t += blockDim.x) td[t] = tds[vds[vtx].term0 + t];
-    __syncthreads();
-    const int g = 1 << glog;
-    const int lane = threadIdx.x & (g - 1);
-    const int gpw = 32 >> glog;                           // lane groups per warp
-    const int sub = (threadIdx.x & 31) >> glog;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // warp-uniform loop (every lane reaches the shuffles); phi >= nout lanes idle
-    for (int64_t base = warp * gpw; base < vd.nout; base += nwarps * gpw) {
-        const int64_t phi = base + sub;
-        const int K = phi < vd.nout ? vd.K : 0;
-        // mixed-radix decode of phi over D(i) (ascending rank, lowest fastest)
-        int64_t off[NT];
+__device__ __forceinline__ void combine(double& b, int& c, double ob, int oc) {
+    // lexicographic min of (cost, C): strict < over increasing C == Fig. 5 line 17
+    if (ob < b || (ob == b && oc < c)) { b = ob; c = oc; }
+}
+
+template <int N>
+struct Log2 { static constexpr int value = 1 + Log2<N / 2>::value; };
+template <>
+struct Log2<1> { static constexpr int value = 0; };
+
+// Coherent L1-cached global load / store.  Explicit ld.global: the table pointers come from
+// shared-memory descriptors, so a plain dereference compiles to a generic LD; an explicit
+// .ca operator makes ptxas build a cache-policy descriptor per load on sm_100a; and
+// ld.global.nc would be unsafe for tables written earlier in the same persistent launch.
+__device__ __forceinline__ double ld(const double* p) {
+    double v;
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_out(double* T, uint16_t* A, int64_t phi, double v, int c) {
+    asm volatile("st.global.f64 [%0], %1;" ::"l"(T + phi), "d"(v) : "memory");
+    asm volatile("st.global.u16 [%0], %1;" ::"l"(A + phi), "h"((unsigned short)c) : "memory");
+}
+
+// Items [first + k*stride + sub, ...) < end for the calling warp (warp-uniform loop).
+template <int NP, int NS, int G>
+__device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td, int64_t first,
+                                        int64_t stride, int64_t end) {
+    constexpr int V = kTile;
+    constexpr int LG = Log2<G>::value, LV = Log2<V>::value;
+    constexpr int S = LG < LV ? LG : LV;          // halving (reduce-scatter) steps
+    constexpr int H = V >> S;                     // values a lane holds afterwards
+    const int lane = threadIdx.x & (G - 1);
+    const int sub = (threadIdx.x & 31) / G;
+    const int q = vd.qstar;
+    int sq[NS > 0 ? NS : 1];                            // host guarantees strides < 2^31
 #pragma unroll
-        for (int t = 0; t < NT; ++t) off[t] = 0;
-        int64_t rem = phi < vd.nout ? phi : 0;
-        for (int q = 0; q < vd.m; ++q) {
-            const int64_t c = rem % vd.radix[q];
-            rem /= vd.radix[q];
+    for (int t = 0; t < NS; ++t) sq[t] = (int)td[NP + t].stride[q];
+
+    for (int64_t base = first; base < end; base += stride) {
+        const int64_t item = base + sub;
+        const bool valid = item < end;
+        const uint32_t it = valid ? (uint32_t)item : 0u;   // host guarantees nitems < 2^31
+        const uint32_t nc = (uint32_t)vd.ncombo;
+        uint32_t rem = it % nc;                             // combos fastest: warps of a CTA
+        const int x0 = (int)(it / nc) * V;                  // share the qstar tile (L1 reuse)
+        const int nb = valid ? min(V, vd.rq - x0) : 0;
+        const double* pp[NP];
+        const double* sp[NS > 0 ? NS : 1];
 #pragma unroll
-            for (int t = 0; t < NT; ++t) off[t] += c * td[t].stride[q];
+        for (int t = 0; t < NP; ++t) pp[t] = td[t].base;
+#pragma unroll
+        for (int t = 0; t < NS; ++t) sp[t] = td[NP + t].base + (int64_t)x0 * sq[t];
+        int64_t obase = 0, ost = 1;
+        for (int c = 0; c < vd.m; ++c) {                    // mixed-radix decode (lowest fastest)
+            const uint32_t r = (uint32_t)vd.radix[c];
+            if (c != q) {
+                const uint32_t v = rem % r;
+                rem /= r;
+                obase += (int64_t)v * ost;
+#pragma unroll
+                for (int t = 0; t < NP; ++t) pp[t] += (int64_t)v * td[t].stride[c];
+#pragma unroll
+                for (int t = 0; t < NS; ++t) sp[t] += (int64_t)v * td[NP + t].stride[c];
+            }
+            ost *= r;
         }
-        const double* ptr[NT];
+        double best[V];
+        int bestC[V];
 #pragma unroll
-        for (int t = 0; t < NT; ++t) ptr[t] = td[t].base + off[t];
-        double best = __longlong_as_double(0x7ff0000000000000ll);   // +inf
-        int bestC = 0x7fffffff;
-        for (int C = lane; C < K; C += g) {
-            double cost = __ldg(ptr[0] + C);
+        for (int j = 0; j < V; ++j) { best[j] = __longlong_as_double(0x7ff0000000000000ll); bestC[j] = 0x7fffffff; }
+        const int Kv = nb > 0 ? vd.K : 0;
+        const int jmax = nb > 0 ? nb - 1 : 0;
+#pragma unroll 2
+        for (int C = lane; C < Kv; C += G) {                // unrolled: loads of 2 C in flight
+            double pre = ld(pp[0] + C);                     // L[C] (term 0 is never in the suffix)
 #pragma unroll
-            for (int t = 1; t < NT; ++t) cost = __dadd_rn(cost, __ldg(ptr[t] + C));
-            if (cost < best) { best = cost; bestC = C; }          // strict <: lowest C in lane
+            for (int t = 1; t < NP; ++t) pre = __dadd_rn(pre, ld(pp[t] + C));
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const int jj = j < jmax ? j : jmax;         // clamp: branch-free partial tiles
+                double cost = pre;
+#pragma unroll
+                for (int t = 0; t < NS; ++t) cost = __dadd_rn(cost, ld(sp[t] + (int64_t)jj * sq[t] + C));
+                if (cost < best[j]) { best[j] = cost; bestC[j] = C; }   // strict <: lowest C
+            }
         }
-        // combine lanes: smaller cost, or equal cost and smaller C
-        for (int o = g >> 1; o > 0; o >>= 1) {
-            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oc = __shfl_xor_sync(0xffffffffu, bestC, o);
-            if (ob < best || (ob == best && oc < bestC)) { best = ob; bestC = oc; }
+        // butterfly reduce-scatter across the G lanes of the group
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int o = G >> (s + 1);
+            const int half = V >> (s + 1);
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int k = 0; k < half; ++k) {
+                const double sb = up ? best[k] : best[k + half];
+                const int sc = up ? bestC[k] : bestC[k + half];
+                double kb = up ? best[k + half] : best[k];
+                int kc = up ? bestC[k + half] : bestC[k];
+                const double rb = __shfl_xor_sync(0xffffffffu, sb, o);
+                const int rc = __shfl_xor_sync(0xffffffffu, sc, o);
+                combine(kb, kc, rb, rc);
+                best[k] = kb;
+                bestC[k] = kc;
+            }
         }
-        if (lane == 0 && K > 0) {
-            vd.T[phi] = best;
-            vd.A[phi] = (uint16_t)bestC;
+#pragma unroll
+        for (int o = G >> (S + 1); o >= 1; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+                const double rb = __shfl_xor_sync(0xffffffffu, best[k], o);
+                const int rc = __shfl_xor_sync(0xffffffffu, bestC[k], o);
+                combine(best[k], bestC[k], rb, rc);
+            }
+        int jbase = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (lane & (G >> (s + 1))) jbase += V >> (s + 1);
+        if ((lane & ((G >> S) - 1)) == 0) {
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+                const int j = jbase + k;
+                if (j < nb) st_out(vd.T, vd.A, obase + (int64_t)(x0 + j) * vd.ostride_q, best[k], bestC[k]);
+            }
         }
     }
 }
 
-// Fallback for vertices with more than kMaxTermsReg summands: offsets recomputed per candidate.
-__global__ void __launch_bounds__(256)
-dp_fill_kernel_many(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ tds, int vtx, int glog) {
-    const VertexDesc& vd = vds[vtx];
+// Generic path (any number of terms, 64-bit strides): one lane group per output phi,
+// offsets recomputed per candidate.  Outputs [first + k*stride + sub, ...) < end.
+__device__ __noinline__ void generic_items(const VertexDesc& vd, const TermDesc* __restrict__ tds, int glog,
+                                           int64_t first, int64_t stride, int64_t end) {
     const int g = 1 << glog;
     const int lane = threadIdx.x & (g - 1);
-    const int gpw = 32 >> glog;
     const int sub = (threadIdx.x & 31) >> glog;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t base = warp * gpw; base < vd.nout; base += nwarps * gpw) {
+    for (int64_t base = first; base < end; base += stride) {
         const int64_t phi = base + sub;
-        const int K = phi < vd.nout ? vd.K : 0;
+        const int K = phi < end ? vd.K : 0;
         int32_t c[kMaxDep];
-        int64_t rem = phi < vd.nout ? phi : 0;
+        int64_t rem = phi < end ? phi : 0;
         for (int q = 0; q < vd.m; ++q) { c[q] = (int32_t)(rem % vd.radix[q]); rem /= vd.radix[q]; }
         double best = __longlong_as_double(0x7ff0000000000000ll);
         int bestC = 0x7fffffff;
@@ -197,7 +305,7 @@ dp_fill_kernel_many(const VertexDesc* __restrict__ vds, const TermDesc* __restri
                 const TermDesc& d = tds[vd.term0 + t];
                 int64_t off = 0;
                 for (int q = 0; q < vd.m; ++q) off += (int64_t)c[q] * d.stride[q];
-                const double x = __ldg(d.base + off + C);
+                const double x = ld(d.base + off + C);
                 cost = t == 0 ? x : __dadd_rn(cost, x);
             }
             if (cost < best) { best = cost; bestC = C; }
@@ -205,55 +313,216 @@ dp_fill_kernel_many(const VertexDesc* __restrict__ vds, const TermDesc* __restri
         for (int o = g >> 1; o > 0; o >>= 1) {
             const double ob = __shfl_xor_sync(0xffffffffu, best, o);
             const int oc = __shfl_xor_sync(0xffffffffu, bestC, o);
-            if (ob < best || (ob == best && oc < bestC)) { best = ob; bestC = oc; }
+            combine(best, bestC, ob, oc);
         }
-        if (lane == 0 && K > 0) {
-            vd.T[phi] = best;
-            vd.A[phi] = (uint16_t)bestC;
+        if (lane == 0 && K > 0) st_out(vd.T, vd.A, phi, best, bestC);
+    }
+}
+
+// shape index: 0..63 = tiled (NP-1)*16 + NS*4 + (log2 G - 2); -1 = generic
+__device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const TermDesc* td_sh,
+                                          const TermDesc* tds_g, int64_t first_warp, int64_t nwarps,
+                                          int64_t i0, int64_t i1) {
+    switch (shape) {
+#define PASE_CASE(NP, NS, LGG)                                                                    \
+    case (NP - 1) * 16 + NS * 4 + (LGG - 2): {                                                    \
+        constexpr int G_ = 1 << LGG, GPW_ = 32 / G_;                                              \
+        tile_items<NP, NS, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1);             \
+        return;                                                                                   \
+    }
+#define PASE_NS(NP, NS) PASE_CASE(NP, NS, 2) PASE_CASE(NP, NS, 3) PASE_CASE(NP, NS, 4) PASE_CASE(NP, NS, 5)
+#define PASE_NP(NP) PASE_NS(NP, 0) PASE_NS(NP, 1) PASE_NS(NP, 2) PASE_NS(NP, 3)
+        PASE_NP(1) PASE_NP(2) PASE_NP(3) PASE_NP(4)
+#undef PASE_NP
+#undef PASE_NS
+#undef PASE_CASE
+        default: {
+            const int gpw = 32 >> vd.glog;
+            generic_items(vd, tds_g, vd.glog, i0 + first_warp * gpw, nwarps * gpw, i1);
         }
     }
+}
+
+// ---- per-vertex launch schedule (PASE_SCHEDULE=launches): one kernel per DP vertex ----
+__global__ void __launch_bounds__(256, 2)
+dp_fill_vertex(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ tds, int vtx) {
+    __shared__ VertexDesc vd;
+    __shared__ TermDesc td[kMaxTermsSh];
+    if (threadIdx.x == 0) vd = vds[vtx];
+    const int nt = min(vds[vtx].nterms, kMaxTermsSh);
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) td[t] = tds[vds[vtx].term0 + t];
+    __syncthreads();
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    run_shape(vd.shape, vd, td, tds, warp, nwarps, 0, vd.shape >= 0 ? vd.nitems : vd.nout);
 }
 
 void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vertex,
                       const VertexDesc& vh, void* stream) {
-    int glog = 0;
-    while ((1 << glog) < vh.K && glog < 5) ++glog;
     const int threads = 256;
-    int64_t blocks = (vh.nout * (1ll << glog) + threads - 1) / threads;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    if (blocks < 1) blocks = 1;
-    cudaStream_t s = (cudaStream_t)stream;
-    switch (vh.nterms) {
-#define PASE_NT(N) case N: dp_fill_kernel<N><<<(unsigned)blocks, threads, 0, s>>>(vd_dev, td_dev, vertex, glog); break;
-        PASE_NT(1) PASE_NT(2) PASE_NT(3) PASE_NT(4) PASE_NT(5) PASE_NT(6) PASE_NT(7) PASE_NT(8)
-#undef PASE_NT
-        default: dp_fill_kernel_many<<<(unsigned)blocks, threads, 0, s>>>(vd_dev, td_dev, vertex, glog);
-    }
+    const int G = 1 << vh.glog;
+    const int64_t units = vh.shape >= 0 ? vh.nitems : vh.nout;
+    int64_t blocks = (units * G + threads - 1) / threads;
+    blocks = blocks > 148 * 8 ? 148 * 8 : (blocks < 1 ? 1 : blocks);
+    dp_fill_vertex<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(vd_dev, td_dev, vertex);
 }
 
-// =====================================================================================
-// K3: back-substitution: phi*(sigma_i) = A(i)[index(phi*|D(i))], i = |V|..1
-// =====================================================================================
-__global__ void backtrack_kernel(const int32_t* __restrict__ sigma, const int32_t* __restrict__ dep_off,
-                                 const int32_t* __restrict__ dep_ids, const VertexDesc* __restrict__ vds,
-                                 int n, int32_t* __restrict__ choice, double* __restrict__ total) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    *total = vds[n - 1].T[0];                              // f(|V|, ∅)
-    for (int i = n - 1; i >= 0; --i) {
-        int64_t idx = 0, stride = 1;
-        for (int a = dep_off[i]; a < dep_off[i + 1]; ++a) {
-            idx += (int64_t)choice[dep_ids[a]] * stride;
-            stride *= vds[i].radix[a - dep_off[i]];
+// ---- persistent schedule (default): one launch runs the whole elimination tree ----------
+//   Tasks (item ranges of one vertex) are claimed in a static order computed on the host by
+//   list-scheduling the task DAG on the CTAs of the grid with critical-path priority (a
+//   topological order, so every task a CTA waits on is held by a running CTA: deadlock-free).
+//   A claimed task waits until pending[vertex] -- the unfinished tasks of the vertex's
+//   children -- reaches zero (relaxed polling, then one ld.acquire); its descriptors are
+//   fetched meanwhile.  A finished task decrements its parent's counter with an acq_rel RMW
+//   after a CTA barrier, so a consumer that acquires the counter observes all child-table
+//   writes (release sequence through pending[]).
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+    uint32_t s;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+    return s;
+}
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ld_relaxed(const int32_t* p) {
+    // polling load: no acquire fence (an acquire invalidates the SM's L1 on every poll,
+    // evicting the working set of the co-resident CTA)
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int atom_add_acq_rel(int32_t* p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+__global__ void __launch_bounds__(256, 2)
+dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ tds,
+              const TaskDesc* __restrict__ tasks, const int32_t* __restrict__ order, int ntasks,
+              int32_t* __restrict__ sched, int64_t* __restrict__ trace) {
+    // sched: [0] claim counter (own 128-B line), [kSchedLine, +n) pending per vertex
+    int32_t* head = sched;
+    int32_t* pending = sched + kSchedLine;
+    __shared__ VertexDesc vd;
+    __shared__ TermDesc td[kMaxTermsSh];
+    __shared__ int s_task;
+    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    int cur = -1;
+    for (;;) {
+        int64_t t_claim = 0, t_start = 0;
+        if (threadIdx.x == 0) {
+            if (trace) t_claim = (int64_t)globaltimer();
+            const int s = atomicAdd(head, 1);
+            s_task = s < ntasks ? order[s] : -1;
         }
-        choice[sigma[i]] = vds[i].A[idx];
+        __syncthreads();
+        const int task = s_task;
+        if (task < 0) break;
+        const TaskDesc tk = tasks[task];
+        if (tk.vtx != cur) {                                // descriptors: static, fetch now
+            if (threadIdx.x == 0) vd = vds[tk.vtx];
+            __syncthreads();
+            const int nt = min(vd.nterms, kMaxTermsSh);
+            for (int k = threadIdx.x; k < nt; k += blockDim.x) td[k] = tds[vd.term0 + k];
+            cur = tk.vtx;
+        }
+        if (threadIdx.x == 0) {                             // wait for the children's tasks
+            if (ld_relaxed(pending + tk.vtx) != 0) {
+                unsigned bo = 32;
+                while (ld_relaxed(pending + tk.vtx) != 0) {
+                    __nanosleep(bo);
+                    bo = bo < 256 ? 2 * bo : 256;
+                }
+            }
+            (void)ld_acquire(pending + tk.vtx);
+            if (trace) t_start = (int64_t)globaltimer();
+        }
+        __syncthreads();
+        run_shape(vd.shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1);
+        __syncthreads();                                    // task's stores precede the release
+        if (threadIdx.x == 0) {
+            if (vd.parent >= 0) atom_add_acq_rel(pending + vd.parent, -1);
+            if (trace) {                                    // PASE_TRACE: per-task timeline
+                trace[4 * task + 0] = ((int64_t)smid() << 32) | (uint32_t)tk.vtx;
+                trace[4 * task + 1] = t_claim;
+                trace[4 * task + 2] = t_start;
+                trace[4 * task + 3] = (int64_t)globaltimer();
+            }
+        }
     }
 }
 
-void launch_backtrack(const int32_t* sigma_dev, const int32_t* dep_off_dev, const int32_t* dep_ids_dev,
-                      const VertexDesc* vd_dev, int n, int32_t* choice_dev, double* total_dev,
-                      void* stream) {
-    backtrack_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(sigma_dev, dep_off_dev, dep_ids_dev, vd_dev, n,
-                                                         choice_dev, total_dev);
+void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, const TaskDesc* tasks_dev,
+                          const int32_t* order_dev, int ntasks, int32_t* sched_dev, int nblocks,
+                          int64_t* trace_dev, void* stream) {
+    dp_persistent<<<(unsigned)nblocks, 256, 0, (cudaStream_t)stream>>>(vd_dev, td_dev, tasks_dev, order_dev,
+                                                                         ntasks, sched_dev, trace_dev);
+}
+
+int persistent_blocks_per_sm() {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_persistent, 256, 0);
+    return nb;
+}
+
+// =====================================================================================
+// K3: back-substitution: phi*(sigma_i) = A(i)[index(phi*|D(i))].  D(i) holds
+// only ancestors of i in the elimination tree, so all vertices of one "back level"
+// (1 + max back level over D(i); the root is level 0) are independent: one CTA walks the
+// levels, a thread per vertex, choices in shared memory.
+// =====================================================================================
+template <bool SMEM>
+__global__ void __launch_bounds__(1024)
+backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt_off, int nlev, int n,
+                 const double* __restrict__ root_T, int32_t* __restrict__ choice, double* __restrict__ total) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // SMEM: records staged once (coalesced), choices kept on chip; only the A(i) reads of
+    // the dependent chain go to memory (L2-resident: the DP has just written them).
+    BtDesc* sh_bt = reinterpret_cast<BtDesc*>(smem_raw);
+    int32_t* sh_choice = reinterpret_cast<int32_t*>(smem_raw + sizeof(BtDesc) * (size_t)n);
+    const BtDesc* bt = SMEM ? sh_bt : bt_g;
+    int32_t* ch = SMEM ? sh_choice : choice;
+    if (SMEM) {
+        const int words = (int)(sizeof(BtDesc) / 4) * n;
+        const int32_t* src = reinterpret_cast<const int32_t*>(bt_g);
+        int32_t* dst = reinterpret_cast<int32_t*>(sh_bt);
+        for (int k = threadIdx.x; k < words; k += blockDim.x) dst[k] = src[k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = root_T[0];             // f(|V|, ∅)
+    for (int lev = 0; lev < nlev; ++lev) {
+        for (int k = bt_off[lev] + threadIdx.x; k < bt_off[lev + 1]; k += blockDim.x) {
+            const BtDesc& d = bt[k];
+            int64_t idx = 0, stride = 1;
+            for (int a = 0; a < d.m; ++a) {
+                idx += (int64_t)ch[d.dep[a]] * stride;
+                stride *= d.radix[a];
+            }
+            ch[d.node] = d.A[idx];
+        }
+        __syncthreads();
+    }
+    if (SMEM)
+        for (int v = threadIdx.x; v < n; v += blockDim.x) choice[v] = sh_choice[v];
+}
+
+void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,
+                      const double* root_T, int32_t* choice_dev, double* total_dev, void* stream) {
+    const size_t smem = (sizeof(BtDesc) + sizeof(int32_t)) * (size_t)n;
+    if (smem <= 48 * 1024)
+        backtrack_kernel<true><<<1, 1024, smem, (cudaStream_t)stream>>>(bt_dev, bt_off_dev, nlev, n, root_T,
+                                                                       choice_dev, total_dev);
+    else
+        backtrack_kernel<false><<<1, 1024, 0, (cudaStream_t)stream>>>(bt_dev, bt_off_dev, nlev, n, root_T,
+                                                                     choice_dev, total_dev);
 }
 
 }  // namespace pase

@@ -62,6 +62,12 @@ struct EdgeDesc {            // cost-table kernel: one per edge
     int64_t woff;            // doubles
 };
 
+struct CostChunk {           // cost-table kernel work unit (one CTA)
+    int32_t item;            // < n: vertex (all of L_v); >= n: edge item - n
+    int32_t row0, nrows;     // edge: rows [row0, row0 + nrows) of W_e (later-endpoint configs)
+    int32_t pad;
+};
+
 struct TermDesc {            // one summand of Eq. 4 for a vertex (L, one W_e, or one child T_j)
     const double* base;      // element(phi, C) = base[sum_q c_q * stride[q] + C]
     int64_t stride[kMaxDep];
@@ -76,17 +82,53 @@ struct VertexDesc {          // one DP vertex (rank i)
     int32_t radix[kMaxDep];  // K of each D(i) coordinate, ascending rank (lowest fastest)
     double* T;               // output table
     uint16_t* A;             // argmin table
+    // tiled schedule: outputs are tiled along coordinate qstar; terms
+    // [0, tstar) do not depend on qstar and are summed once per C per tile (hoisted prefix).
+    int32_t qstar;           // tiled coordinate (-1: root, D(i) = ∅)
+    int32_t tstar;           // first term depending on qstar
+    int32_t rq;              // radix of qstar (1 for the root)
+    int32_t ntile;           // tiles along qstar = ceil(rq / kTile)
+    int64_t ostride_q;       // output stride of qstar
+    int64_t ncombo;          // nout / rq
+    int64_t nitems;          // ncombo * ntile
+    int32_t glog;            // log2 lane-group size
+    int32_t shape;           // tiled variant (NP-1)*16 + NS*4 + (glog-2), or -1 = generic kernel
+    int32_t ntasks;          // persistent schedule: tasks of this vertex ...
+    int32_t task0;           // ... with ids [task0, task0 + ntasks)
+    int32_t parent;          // rank of the elimination-tree parent (-1: root)
+    int32_t items_per_task;  // host-side task sizing
+    int32_t pad;
+};
+constexpr int kSchedLine = 32;   // int32 words per 128-B line (scheduler control block)
+constexpr int kMaxTermsSh = 8;   // terms staged in shared memory (tiled shapes use <= 7)
+
+struct TaskDesc {            // persistent schedule: item range [i0, i1) of vertex vtx
+    int32_t vtx, pad;
+    int64_t i0, i1;
+};
+constexpr int kTile = 8;     // max outputs per lane group along qstar
+constexpr int kCostRows = 64;  // edge-table rows per cost-table CTA
+
+struct BtDesc {               // back-substitution record of one rank, in back-level order
+    const uint16_t* A;       // argmin table A(i)
+    int32_t node;            // sigma_i
+    int32_t m;               // |D(i)|
+    int32_t dep[kMaxDep];    // D(i) node ids, ascending rank
+    int32_t radix[kMaxDep];
 };
 
 // kernels.cu entry points (host-side launchers)
 void launch_cost_tables(const pase_node* nodes_dev, const int32_t* K_dev, const int64_t* cfg_off_dev,
                         const int32_t* cfg_dev, const int64_t* loff_dev, int n,
-                        const EdgeDesc* edges_dev, int m, const int64_t* item_off_dev,
-                        int64_t total, double r, double* L_dev, double* W_dev, void* stream);
+                        const EdgeDesc* edges_dev, const CostChunk* chunks_dev, int nchunks,
+                        double r, double* L_dev, double* W_dev, void* stream);
 void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vertex,
                       const VertexDesc& vd_host, void* stream);
-void launch_backtrack(const int32_t* sigma_dev, const int32_t* dep_off_dev, const int32_t* dep_ids_dev,
-                      const VertexDesc* vd_dev, int n, int32_t* choice_dev, double* total_dev,
-                      void* stream);
+void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, const TaskDesc* tasks_dev,
+                          const int32_t* order_dev, int ntasks, int32_t* sched_dev, int nblocks,
+                          int64_t* trace_dev, void* stream);
+int persistent_blocks_per_sm();
+void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,
+                      const double* root_T, int32_t* choice_dev, double* total_dev, void* stream);
 
 }  // namespace pase

@@ -86,7 +86,8 @@ class pase_stats(C.Structure):
 
 EXPORTS = ["pase_create", "pase_solve", "pase_get_stats", "pase_last_error", "pase_destroy",
            "pase_get_configs", "pase_get_order", "pase_get_cost_tables", "pase_get_dp_table",
-           "pase_table_entries", "pase_set_cost_tables", "pase_set_profiling", "pase_get_unique_id"]
+           "pase_table_entries", "pase_set_cost_tables", "pase_set_profiling", "pase_get_unique_id",
+           "pase_get_trace"]
 
 _lib = None
 
@@ -123,6 +124,8 @@ def load(path: str = SO):
     L.pase_set_cost_tables.argtypes = [ctx_p, P(C.c_double), P(C.c_double)]
     L.pase_set_profiling.argtypes = [ctx_p, C.c_int32]
     L.pase_get_unique_id.argtypes = [C.c_void_p]
+    L.pase_get_trace.argtypes = [ctx_p, P(C.c_int64), C.c_int64]
+    L.pase_get_trace.restype = C.c_int64
     for f in ("pase_create", "pase_solve", "pase_get_stats", "pase_get_configs", "pase_get_order",
               "pase_get_cost_tables", "pase_get_dp_table", "pase_set_cost_tables", "pase_set_profiling",
               "pase_get_unique_id"):
@@ -302,6 +305,20 @@ class Context:
         A = np.zeros(n, np.uint16)
         self._chk(self._L.pase_get_dp_table(self._h, rank, _ptr(T, C.c_double), _ptr(A, C.c_uint16)))
         return T, A
+
+    def trace(self) -> np.ndarray:
+        """PASE_TRACE=1 timeline of the last solve: rows (rank, smid, t_claim, t_start, t_end) ns."""
+        n = self._L.pase_get_trace(self._h, None, 0)
+        if n <= 0:
+            return np.zeros((0, 5), np.int64)
+        buf = np.zeros(4 * n, np.int64)
+        self._L.pase_get_trace(self._h, _ptr(buf, C.c_int64), n)
+        r = buf.reshape(n, 4)
+        out = np.zeros((n, 5), np.int64)
+        out[:, 0] = r[:, 0] & 0xffffffff
+        out[:, 1] = r[:, 0] >> 32
+        out[:, 2:] = r[:, 1:]
+        return out
 
     def set_cost_tables(self, Ls: Sequence[np.ndarray], Ws: Sequence[np.ndarray]) -> None:
         L = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float64).ravel() for x in Ls]))

@@ -546,6 +546,8 @@ BENCH_GRAPHS = {
     "rnnlm": (rnnlm_unrolled, 64),
     "gnmt": (gnmt_unrolled, 64),
     "transformer": (transformer, 64),
+    # latency microbenchmark (not a paper config): a 200-vertex path, |D(i)| = 1, K = 6
+    "chain200": (lambda: mlp(layers=200), 4),
 }
 
 

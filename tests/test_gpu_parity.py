@@ -170,3 +170,18 @@ def test_separable_r0_full_scale():
         Ls, Ws = ctx.cost_tables()
     assert all((w == 0).all() for w in Ws)
     assert list(r["config_index"]) == [int(np.argmin(l)) for l in Ls]
+
+
+@pytest.mark.parametrize("schedule,no_graph", [("launches", "0"), ("persistent", "1"), ("launches", "1")])
+def test_alternate_schedules(schedule, no_graph, monkeypatch):
+    """The per-vertex launch schedule and the un-captured (PASE_NO_GRAPH) paths give the
+    same bit-exact tables as the default persistent CUDA-graph schedule."""
+    monkeypatch.setenv("PASE_SCHEDULE", schedule)
+    monkeypatch.setenv("PASE_NO_GRAPH", no_graph)
+    for name in ("alexnet", "inception_v3", "transformer"):
+        g, p = zoo.bench_graph(name)
+        run_pair(g, p, "exact_p")
+    g, p = zoo.random_chain_graph(9, 4, kmax=9, extra_p=0.6)
+    K = np.array([len(c) for c in O.configs(g, p, O.LE_P)], np.int32)
+    Ls, Ws = random_costs(g, K, 99, "real")
+    run_pair(g, p, "le_p", Ls, Ws)
