@@ -1,13 +1,13 @@
-# GPU round: parity tests, smoke, bench, launch list, one full ncu capture of the top dp_fill.
+# GPU round: parity tests, smoke, bench (default + LE_P), launch list, one full ncu capture
+# of the dominant kernel (dp_persistent) and one of the cost-table kernel.
 set -x
 cd $GRAFT_REPO_ROOT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
-PASE_TIMING=1 timeout 300 python scripts/profile_one.py transformer --solves 3 2>&1 | tail -3
-PASE_TIMING=1 timeout 300 python scripts/profile_one.py transformer --solves 3 2>&1 | tail -3
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
 timeout 600 python bench.py --steps 100 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
 timeout 600 python bench.py --workload transformer_le --steps 20 --warmup 3 --e2e-steps 3 > gpurun_out/bench_le.json 2> gpurun_out/bench_le.err; tail -3 gpurun_out/bench_le.err; cat gpurun_out/bench_le.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python scripts/profile_one.py transformer --solves 3 > gpurun_out/ncu_launches.log 2>&1; tail -2 gpurun_out/ncu_launches.log
-R=$(python scripts/profile_one.py transformer --top)
-PASE_NO_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:dp_fill --launch-skip $R --launch-count 1 -o gpurun_out/prof_top -f python scripts/profile_one.py transformer > gpurun_out/ncu_full.log 2>&1; tail -3 gpurun_out/ncu_full.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1; tail -2 gpurun_out/ncu_launches.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:dp_persistent --launch-skip 2 --launch-count 1 -o gpurun_out/prof_dp -f python scripts/profile_one.py transformer --solves 3 > gpurun_out/ncu_full.log 2>&1; tail -2 gpurun_out/ncu_full.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:dp_persistent --launch-skip 2 --launch-count 1 -o gpurun_out/prof_dp_le -f python scripts/profile_one.py transformer_le --solves 3 > gpurun_out/ncu_full_le.log 2>&1; tail -2 gpurun_out/ncu_full_le.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:cost_tables --launch-skip 2 --launch-count 1 -o gpurun_out/prof_cost -f python scripts/profile_one.py transformer --solves 3 > gpurun_out/ncu_cost.log 2>&1; tail -2 gpurun_out/ncu_cost.log
