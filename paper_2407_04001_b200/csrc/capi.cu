@@ -117,10 +117,12 @@ bool trace_on() {
     return t && t[0] == '1';
 }
 
-// lane-group size: each lane should own >= ~4 values of C (K=28 -> 4 lanes, K=205 -> 32)
+// lane-group size: each lane should own >= ~8 values of C (K=28 -> 4 lanes, K=84 -> 8,
+// K=205 -> 16, K=456 -> 32): fewer lanes per item amortise the per-item decode and the
+// cross-lane reduction over more candidates.
 int lane_group_log2(int K) {
     int g = 2;
-    while (g < 5 && (1 << (g + 1)) * 4 <= K) ++g;
+    while (g < 5 && (1 << (g + 1)) * 8 <= K) ++g;
     return g;
 }
 
