@@ -57,6 +57,12 @@ typedef enum {
  * achievable product <= p.  LE_P: prod c_k <= p (the set-builder of P:204-205). */
 typedef enum { PASE_CFG_EXACT_P = 0, PASE_CFG_LE_P = 1 } pase_cfg_policy;
 
+/* Vertex ordering: SortNodes (Fig. 4; the paper's DP-Alg) or breadth-first
+ * (Table 1's "BF" baseline) -- same Eq. 4 DP over either; the BF
+ * ordering's dependent sets grow large on Inception/Transformer and trip the size guard
+ * (PASE_ERR_RESOURCE, the paper's "OOM"). */
+typedef enum { PASE_ORDER_SORTNODES = 0, PASE_ORDER_BFS = 1 } pase_ordering;
+
 /* One vertex = one layer with its iteration space. */
 typedef struct {
     int32_t n_dims;                        /* 1..PASE_MAX_DIMS */
@@ -93,7 +99,7 @@ typedef struct {
     double flops_per_device;           /* F, FLOP/s */
     double link_bandwidth;             /* B, bytes/s (may be +inf: r = 0) */
     int32_t cfg_policy;                /* pase_cfg_policy */
-    int32_t reserved0;
+    int32_t ordering;                  /* pase_ordering (0 = SortNodes) */
     uint64_t table_budget_bytes;       /* size guard over all DP tables; 0 = 64 GiB */
     uint64_t redundant_below_bytes;    /* multi-GPU: tables below this are computed on every rank */
     int32_t cuda_device;               /* device ordinal for this process; < 0 = host-only planning

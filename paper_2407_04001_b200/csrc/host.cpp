@@ -139,8 +139,26 @@ void enumerate(const pase_node& x, int p, int policy, std::vector<int32_t>& rows
 // ---------------------------------------------------------------- a3
 // SortNodes (Fig. 4) with bitset d-sets.  Reading C: v.d <- (v.d ∪ sigma_i.d) - {sigma_i, v};
 // reading D: ties -> smallest node id.
+// Breadth-first order: source = smallest node id, neighbours by increasing id.
+std::vector<int32_t> bfs_order(int n, const std::vector<pase_edge>& edges) {
+    std::vector<std::vector<int32_t>> nb(n);
+    for (const pase_edge& e : edges) { nb[e.src].push_back(e.dst); nb[e.dst].push_back(e.src); }
+    for (auto& l : nb) { std::sort(l.begin(), l.end()); l.erase(std::unique(l.begin(), l.end()), l.end()); }
+    std::vector<int32_t> order;
+    std::vector<char> seen(n, 0);
+    order.push_back(0);
+    seen[0] = 1;
+    for (size_t h = 0; h < order.size(); ++h)
+        for (int y : nb[order[h]])
+            if (!seen[y]) { seen[y] = 1; order.push_back(y); }
+    return order;
+}
+
+// SortNodes (Fig. 4).  With `fixed` non-empty, the vertex of step i is fixed[i] instead of
+// the argmin of line 5: the update of line 8 then yields D(i) for that ordering too
+// (Theorem 2's induction, does not use the argmin) -- the BFS baseline.
 void sort_nodes(int n, const std::vector<pase_edge>& edges, std::vector<int32_t>& sigma,
-                std::vector<std::vector<int32_t>>& dep_nodes) {
+                std::vector<std::vector<int32_t>>& dep_nodes, const std::vector<int32_t>& fixed = {}) {
     const int W = (n + 63) / 64;
     std::vector<uint64_t> d((size_t)n * W, 0);
     auto bit = [&](int v, int x) -> uint64_t& { return d[(size_t)v * W + x / 64]; };
@@ -161,8 +179,10 @@ void sort_nodes(int n, const std::vector<pase_edge>& edges, std::vector<int32_t>
     std::vector<uint64_t> di(W);
     for (int i = 0; i < n; ++i) {                         // line 4
         int u = -1;
-        for (int v = 0; v < n; ++v)                       // line 5: argmin |u.d|, smallest id first
-            if (unseq[v] && (u < 0 || card[v] < card[u])) u = v;
+        if (!fixed.empty()) u = fixed[i];
+        else
+            for (int v = 0; v < n; ++v)                   // line 5: argmin |u.d|, smallest id first
+                if (unseq[v] && (u < 0 || card[v] < card[u])) u = v;
         sigma[i] = u;
         unseq[u] = 0;                                     // line 6
         std::copy(d.begin() + (size_t)u * W, d.begin() + (size_t)(u + 1) * W, di.begin());
@@ -186,6 +206,7 @@ pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* mach,
     if (p < 1 || p > 4096) { err = fmt("p = %lld out of range [1, 4096]", p); return PASE_ERR_INVALID; }
     if (!mach) { err = "machine is NULL"; return PASE_ERR_INVALID; }
     if (mach->cfg_policy != PASE_CFG_EXACT_P && mach->cfg_policy != PASE_CFG_LE_P) { err = "bad cfg_policy"; return PASE_ERR_INVALID; }
+    if (mach->ordering != PASE_ORDER_SORTNODES && mach->ordering != PASE_ORDER_BFS) { err = "bad ordering"; return PASE_ERR_INVALID; }
     if (!(mach->flops_per_device > 0) || !(mach->link_bandwidth > 0)) { err = "F and B must be > 0"; return PASE_ERR_INVALID; }
     pase_status st = validate(g, err);
     if (st) return st;
@@ -217,7 +238,8 @@ pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* mach,
 
     // a3
     std::vector<std::vector<int32_t>> dn;
-    sort_nodes(n, P.edges, P.sigma, dn);
+    if (mach->ordering == PASE_ORDER_BFS) sort_nodes(n, P.edges, P.sigma, dn, bfs_order(n, P.edges));
+    else sort_nodes(n, P.edges, P.sigma, dn);
     P.rank.assign(n, 0);
     for (int i = 0; i < n; ++i) P.rank[P.sigma[i]] = i;
     P.dep.assign(n, {});
@@ -293,6 +315,15 @@ pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* mach,
     }
     P.entries = 0;
     for (int i = 0; i < n; ++i) P.entries += (uint64_t)P.tsize[i];
+    // size guard (Table 1 "OOM"): DP + argmin tables
+    const uint64_t budget = mach->table_budget_bytes ? mach->table_budget_bytes : (64ull << 30);
+    if ((uint64_t)P.toff[n] * 10ull > budget) {
+        char buf[200];
+        std::snprintf(buf, sizeof buf, "size guard: DP tables need %.3f GB > budget %.3f GB (M = %d, K = %d)",
+                      (double)P.toff[n] * 10.0 / 1e9, (double)budget / 1e9, P.max_dep, P.max_k);
+        err = buf;
+        return PASE_ERR_RESOURCE;
+    }
     P.loff.assign(n + 1, 0);
     for (int v = 0; v < n; ++v) P.loff[v + 1] = P.loff[v] + P.K[v];
     P.woff.assign(m + 1, 0);

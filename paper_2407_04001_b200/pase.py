@@ -24,6 +24,7 @@ PASE_CFG_EXACT_P, PASE_CFG_LE_P = 0, 1
 STATUS = {0: "PASE_OK", 1: "PASE_ERR_INVALID", 2: "PASE_ERR_RESOURCE", 3: "PASE_ERR_CUDA",
           4: "PASE_ERR_NCCL", 5: "PASE_ERR_STATE"}
 POLICIES = {"exact_p": PASE_CFG_EXACT_P, "le_p": PASE_CFG_LE_P}
+ORDERINGS = {"sortnodes": 0, "bfs": 1}
 
 
 class pase_node(C.Structure):
@@ -58,7 +59,7 @@ class pase_machine(C.Structure):
         ("flops_per_device", C.c_double),
         ("link_bandwidth", C.c_double),
         ("cfg_policy", C.c_int32),
-        ("reserved0", C.c_int32),
+        ("ordering", C.c_int32),
         ("table_budget_bytes", C.c_uint64),
         ("redundant_below_bytes", C.c_uint64),
         ("cuda_device", C.c_int32),
@@ -185,10 +186,11 @@ def marshal_graph(graph: dict):
 def make_machine(flops: float = 1e13, bandwidth: float = 1e10, policy: int = PASE_CFG_EXACT_P,
                  device: int = 0, stream: Optional[int] = None, rank: int = 0, world: int = 1,
                  uid: Optional[bytes] = None, table_budget: int = 0,
-                 redundant_below: int = 4 << 20) -> pase_machine:
+                 redundant_below: int = 4 << 20, ordering: int = 0) -> pase_machine:
     m = pase_machine()
     m.flops_per_device, m.link_bandwidth = float(flops), float(bandwidth)
     m.cfg_policy = int(policy)
+    m.ordering = int(ordering)
     m.table_budget_bytes = int(table_budget)
     m.redundant_below_bytes = int(redundant_below)
     m.cuda_device, m.rank, m.world = int(device), int(rank), int(world)
@@ -204,7 +206,7 @@ class Context:
     def __init__(self, graph: dict, p: int, policy="exact_p", flops: Optional[float] = None,
                  bandwidth: Optional[float] = None, device: int = 0, stream: Optional[int] = None,
                  rank: int = 0, world: int = 1, uid: Optional[bytes] = None, table_budget: int = 0,
-                 redundant_below: int = 4 << 20):
+                 redundant_below: int = 4 << 20, ordering="sortnodes"):
         L = load()
         mach_d = graph.get("machine") or {}
         flops = flops if flops is not None else mach_d.get("flops", 1e13)
@@ -213,8 +215,9 @@ class Context:
         self.graph = graph
         self.n, self.m = len(graph["nodes"]), len(graph["edges"])
         g, self._keep = marshal_graph(graph)
+        order = ORDERINGS[ordering] if isinstance(ordering, str) else int(ordering)
         self._mach = make_machine(flops, bandwidth, pol, device, stream, rank, world, uid, table_budget,
-                                  redundant_below)
+                                  redundant_below, order)
         h = C.c_void_p()
         st = L.pase_create(C.byref(g), int(p), C.byref(self._mach), C.byref(h))
         if st != 0:

@@ -142,3 +142,43 @@ def test_solve_needs_device(lib):
     with pytest.raises(pase.PaseError) as ei:
         ctx.solve()
     assert ei.value.status == 5
+
+
+def test_bfs_ordering_plan_matches_oracle(lib):
+    """f1: the BFS ordering's dependent sets from the incremental update equal
+    the oracle's definitional D(i) for that ordering; the tree rule still gives S(i)."""
+    for name in ("mlp", "alexnet", "rnnlm"):
+        g, p = zoo.bench_graph(name)
+        ctx = pase.Context(g, p, device=-1, ordering="bfs")
+        K = ctx.K()
+        n = len(K)
+        P = O.Problem(g, K, [np.zeros(k) for k in K], [np.zeros((K[e["src"]], K[e["dst"]])) for e in g["edges"]])
+        sb = P.bfs_order()
+        sigma, deps, parent = ctx.order()
+        assert list(sigma) == list(sb)
+        rank = {int(v): i for i, v in enumerate(sigma)}
+        for i in range(n):
+            s = P.sets(sigma, i)
+            assert set(deps[i]) == s["D"]
+            kids = [j for j in range(n) if parent[j] == i]
+            assert sorted(max(rank[v] for v in comp) for comp in s["S"]) == kids
+    for seed in range(40):
+        g = zoo.random_model_graph(2 + seed % 10, seed)
+        ctx = pase.Context(g, 4, device=-1, ordering="bfs")
+        P = O.Problem(g, ctx.K(), [np.zeros(k) for k in ctx.K()],
+                      [np.zeros((ctx.K()[e["src"]], ctx.K()[e["dst"]])) for e in g["edges"]])
+        sigma, deps, _ = ctx.order()
+        assert list(sigma) == list(P.bfs_order())
+        for i in range(len(sigma)):
+            assert set(deps[i]) == P.sets(sigma, i)["D"]
+
+
+def test_bfs_ordering_oom_on_inception(lib):
+    """Table 1: BF ordering runs out of memory on InceptionV3 -- here the size
+    guard reports PASE_ERR_RESOURCE with M and K; SortNodes plans it in a few MB."""
+    g = zoo.inception_v3()
+    with pytest.raises(pase.PaseError) as ei:
+        pase.Context(g, 8, device=-1, ordering="bfs")
+    assert ei.value.status == 2 and "K =" in str(ei.value)
+    ctx = pase.Context(g, 8, device=-1)
+    assert ctx.stats()["table_entries"] * 10 < 1e9

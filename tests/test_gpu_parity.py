@@ -23,17 +23,18 @@ def rel_eq(a, b, tol=1e-12):
     return abs(a - b) <= tol * max(1.0, abs(a), abs(b))
 
 
-def run_pair(graph, p, policy="exact_p", Ls=None, Ws=None, tables=True, oracle_threads=THREADS):
+def run_pair(graph, p, policy="exact_p", Ls=None, Ws=None, tables=True, oracle_threads=THREADS,
+             ordering="sortnodes"):
     """Solve with the GPU and the oracle on the same inputs; compare everything."""
     pol = pase.POLICIES[policy]
-    ctx = pase.Context(graph, p, policy=policy, device=0)
+    ctx = pase.Context(graph, p, policy=policy, device=0, ordering=ordering)
     if Ls is None:
         P = O.Problem.from_model(graph, p, pol)
     else:
         P = O.Problem(graph, np.array([len(x) for x in Ls], np.int32), Ls, Ws)
         ctx.set_cost_tables(Ls, Ws)
     g = ctx.solve()
-    o = P.dp(threads=oracle_threads, want_tables=tables)
+    o = P.dp(order=1 if ordering == "bfs" else 0, threads=oracle_threads, want_tables=tables)
     assert np.array_equal(ctx.K(), P.K)
     # a5: cost tables bitwise
     gL, gW = ctx.cost_tables()
@@ -185,3 +186,18 @@ def test_alternate_schedules(schedule, no_graph, monkeypatch):
     K = np.array([len(c) for c in O.configs(g, p, O.LE_P)], np.int32)
     Ls, Ws = random_costs(g, K, 99, "real")
     run_pair(g, p, "le_p", Ls, Ws)
+
+
+def test_bfs_ordering_gpu():
+    """f1: the same GPU DP over the breadth-first ordering -- bitwise equal to
+    the oracle's Fig. 5 DP over that ordering, and the same optimum as SortNodes."""
+    for name in ("mlp", "alexnet", "rnnlm"):
+        g, p = zoo.bench_graph(name)
+        gb, _, _ = run_pair(g, p, "exact_p", ordering="bfs")
+        gs = pase.solve(g, p)
+        assert rel_eq(gb["cost"], gs["cost"])
+    for seed in range(20):
+        g, p = zoo.random_chain_graph(2 + seed % 7, 500 + seed, kmax=6, extra_p=0.3)
+        K = np.array([len(c) for c in O.configs(g, p, O.LE_P)], np.int32)
+        Ls, Ws = random_costs(g, K, seed, "real")
+        run_pair(g, p, "le_p", Ls, Ws, ordering="bfs")
