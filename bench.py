@@ -168,20 +168,26 @@ def main():
     from paper_2407_04001_b200 import pase, zoo
     torch.cuda.set_device(local_rank)
     dist = None
-    uid = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        buf = [pase.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(buf, src=0)
-        uid = buf[0]
     key, p, policy, desc = WORKLOADS[args.workload]
     graph = zoo.bench_graph(key)[0]
     stream = torch.cuda.Stream()
     flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device="cuda")
 
-    ctx = pase.Context(graph, p, policy=policy, device=local_rank, stream=stream.cuda_stream,
-                       rank=rank, world=world, uid=uid)
+    def make_ctx():
+        # one rank per GPU; a group exchanges CUDA-IPC handles over torch.distributed, then
+        # the DP kernel moves partitions over NVLink itself (pase_connect)
+        c = pase.Context(graph, p, policy=policy, device=local_rank, stream=stream.cuda_stream,
+                         rank=rank, world=world)
+        if world > 1:
+            hs = [None] * world
+            dist.all_gather_object(hs, c.export_handle())
+            c.connect(hs)
+        return c
+
+    ctx = make_ctx()
     st0 = ctx.stats()
     cand = int(st0["candidates"])
     for _ in range(args.warmup):
@@ -227,8 +233,7 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        with pase.Context(graph, p, policy=policy, device=local_rank, stream=stream.cuda_stream,
-                          rank=rank, world=world, uid=uid) as c2:
+        with make_ctx() as c2:
             c2.solve()
         e1.record(stream)
         e1.synchronize()

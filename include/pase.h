@@ -41,7 +41,8 @@ extern "C" {
 #define PASE_MAX_DIMS 8      /* iteration-space dimensions per vertex */
 #define PASE_MAX_HALO 4      /* conv halo (spatial, filter) pairs per vertex */
 #define PASE_MAX_DEP 12      /* max |D(i)| (M); larger -> PASE_ERR_RESOURCE */
-#define PASE_UID_BYTES 128   /* ncclUniqueId size */
+#define PASE_HANDLE_BYTES 256 /* pase_export_handle blob */
+#define PASE_MAX_WORLD 8     /* search GPUs in one group */
 
 typedef enum {
     PASE_OK = 0,
@@ -101,13 +102,15 @@ typedef struct {
     int32_t cfg_policy;                /* pase_cfg_policy */
     int32_t ordering;                  /* pase_ordering (0 = SortNodes) */
     uint64_t table_budget_bytes;       /* size guard over all DP tables; 0 = 64 GiB */
-    uint64_t redundant_below_bytes;    /* multi-GPU: tables below this are computed on every rank */
+    uint64_t redundant_below_bytes;    /* multi-GPU: tables smaller than this are computed on every
+                                          rank; bigger ones are partitioned */
     int32_t cuda_device;               /* device ordinal for this process; < 0 = host-only planning
                                           context (a1-a4 + stats + introspection; pase_solve and the
                                           table hooks return PASE_ERR_STATE; no device is touched) */
-    int32_t rank, world;               /* search GPUs G (1, 2, 4, 8); world = 1: single GPU */
-    int32_t reserved1;
-    const void* nccl_unique_id;        /* PASE_UID_BYTES bytes, same on every rank; NULL if world == 1 */
+    int32_t rank, world;               /* search GPUs G in [1, PASE_MAX_WORLD]; world = 1: single GPU */
+    int32_t virtual_ranks;             /* 1: all ranks of the group share one device (testing):
+                                          each rank's persistent grid uses 1/world of the SMs */
+    const void* reserved;              /* must be NULL */
     void* cuda_stream;                 /* cudaStream_t to run on; NULL = library-owned stream */
 } pase_machine;
 
@@ -186,8 +189,28 @@ int64_t pase_get_trace(const pase_ctx* ctx, int64_t* out, int64_t cap);
 /* Time the solve phases separately on the next pase_solve (adds syncs; default off). */
 pase_status pase_set_profiling(pase_ctx* ctx, int32_t enable);
 
-/* NCCL unique id for multi-GPU contexts (rank 0 calls it and broadcasts the bytes). */
-pase_status pase_get_unique_id(void* uid_out /* PASE_UID_BYTES */);
+/* ---- split solve (a multi-GPU group launches every rank before waiting on any) ---------- */
+pase_status pase_launch(pase_ctx* ctx);       /* enqueue one solve on the context's stream */
+pase_status pase_finish(pase_ctx* ctx, int32_t* configs_out, int32_t* config_index_out,
+                        double* total_cost_out);   /* wait for it; outputs as pase_solve */
+
+/* ---- multi-GPU group (world > 1) -------------------------------------
+ * Every rank creates its context with the same graph, p and machine (except rank /
+ * cuda_device), exports a handle, the caller exchanges the world handles (e.g. an all-gather
+ * over torch.distributed) and passes them, ordered by rank, to pase_connect.  Big DP tables
+ * are partitioned by their highest-rank coordinate; the DP kernel writes the partitions other
+ * ranks need directly into their tables over NVLink (CUDA IPC peer memory) and signals them
+ * with system-scope atomics: no separate collective.  Contexts of one process on one device
+ * (virtual_ranks = 1) exercise the same path on a single GPU.  pase_solve on a group context
+ * must be called by every rank (the solve contains two group barriers). */
+pase_status pase_export_handle(const pase_ctx* ctx, void* blob /* PASE_HANDLE_BYTES */);
+pase_status pase_connect(pase_ctx* ctx, const void* blobs /* world * PASE_HANDLE_BYTES */);
+
+/* Schedule introspection (also on host-only contexts): per DP rank i, vinfo[4i..4i+3] =
+ * {partitioned, broadcast flags, this rank's task count, initial pending counter}; tasks =
+ * this rank's {rank i, first item, end item} triples; order = claim order.  Returns the task
+ * count (arrays may be NULL). */
+int64_t pase_get_schedule(const pase_ctx* ctx, int32_t* vinfo, int64_t* tasks, int32_t* order);
 
 #ifdef __cplusplus
 }

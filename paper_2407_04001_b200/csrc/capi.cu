@@ -1,8 +1,9 @@
 // capi.cu -- the C ABI of include/pase.h: context lifecycle, device memory, the solve
-// schedule recorded once as a CUDA graph (cost tables -> DP fill over the elimination
-// tree, children before parents, independent subtrees concurrent -> back-substitution ->
-// D2H of the strategy), and the introspection hooks.
+// schedule recorded once as a CUDA graph (cost tables -> [group barrier] -> persistent DP
+// over the elimination tree -> [group barrier] -> back-substitution -> D2H of the strategy),
+// multi-GPU peer connection, and the introspection hooks.
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <chrono>
@@ -10,7 +11,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
-#include <queue>
 #include <string>
 #include <vector>
 
@@ -26,10 +26,12 @@ struct pase_ctx {
     pase_machine mach{};
     std::string err;
     int dev = 0;
+    int world = 1, rank = 0;
+    bool virtual_ranks = false;             // all ranks of the group share this device
     cudaStream_t stream = nullptr;
     bool own_stream = false;
-    std::vector<cudaStream_t> aux;          // fork streams for concurrent subtrees
-    // device memory
+    std::vector<cudaStream_t> aux;          // fork streams (per-vertex launch schedule)
+    // pool 1: inputs, cost tables, DP tables (T/A written by peers), descriptors
     void* pool = nullptr;
     size_t pool_bytes = 0;
     pase_node* d_nodes = nullptr;
@@ -46,26 +48,38 @@ struct pase_ctx {
     uint16_t* d_A = nullptr;
     VertexDesc* d_vd = nullptr;
     TermDesc* d_td = nullptr;
-    pase::TaskDesc* d_tasks = nullptr;
-    int32_t* d_sched = nullptr;             // scheduler state (kernels.cu dp_persistent)
-    int32_t* d_order = nullptr;             // static task claim order
-    int32_t* d_sched_init = nullptr;        // its solve-start image (leaves queued)
-    size_t sched_bytes = 0;
-    int64_t* d_trace = nullptr;             // PASE_TRACE=1: 4 int64 per persistent task
-    int ntasks = 0, nblocks = 0;
-    bool persistent = true;
     pase::BtDesc* d_bt = nullptr;
     int32_t* d_bt_off = nullptr;
     int nbtlev = 0;
     int32_t* d_choice = nullptr;
     double* d_total = nullptr;
+    // pool 2: scheduler (pending counters written by peers), tasks, claim order, trace
+    void* pool2 = nullptr;
+    size_t pool2_bytes = 0;
+    int32_t* d_sched = nullptr;             // [0] claim counter | [kSchedLine, +n) pending
+    int32_t* d_sched_init = nullptr;        // its solve-start image
+    size_t sched_bytes = 0;
+    int32_t* d_bar = nullptr;               // [0] arrivals, [kSchedLine] epoch, [2 kSchedLine] error
+    pase::TaskDesc* d_tasks = nullptr;
+    int32_t* d_order = nullptr;
+    int64_t* d_trace = nullptr;             // PASE_TRACE=1: 4 int64 per persistent task
+    int ntasks = 0, nblocks = 0;
+    int64_t total_tasks = 0;
+    bool persistent = true;
+    // multi-GPU
+    pase::Peers peers{};
+    bool connected = false;
+    std::vector<void*> ipc_opened;
     // host mirrors
     std::vector<VertexDesc> vd;
     std::vector<TermDesc> td;
+    pase::SchedPlan sp;
     int32_t* h_choice = nullptr;            // pinned
     double* h_total = nullptr;              // pinned
+    int32_t* h_err = nullptr;               // pinned
     bool override_tables = false;
     bool solved = false;
+    bool launched = false;
     bool no_graph = false;
     int profiling = 0;
     cudaGraphExec_t exec = nullptr;
@@ -101,16 +115,6 @@ std::vector<pase::CostChunk> cost_chunks(const Plan& P) {
     for (int v = 0; v < P.n; ++v) ch.push_back({v, 0, P.K[v], 0});
     return ch;
 }
-int64_t nchunks_of(const Plan& P) { return (int64_t)cost_chunks(P).size(); }
-
-// Upper bound of persistent tasks (each vertex gets <= kTasksPerBlock * nblocks + 1 tasks).
-constexpr int kTasksPerBlock = 4;
-int64_t max_tasks_of(const Plan& P, int nblocks) {
-    int64_t t = 0;
-    for (int i = 0; i < P.n; ++i)
-        t += std::min<int64_t>(P.tsize[i], (int64_t)kTasksPerBlock * std::max(nblocks, 1) + 1);
-    return std::max<int64_t>(t, 1);
-}
 
 bool trace_on() {
     const char* t = std::getenv("PASE_TRACE");
@@ -126,17 +130,36 @@ int lane_group_log2(int K) {
     return g;
 }
 
-// Carve all device buffers out of one allocation.
-pase_status allocate(pase_ctx* ctx) {
+struct Item { void** ptr; size_t bytes; };
+
+// Carve items out of one allocation (base == nullptr for host-only contexts: offsets only).
+pase_status carve(pase_ctx* ctx, std::vector<Item>& items, void** base, size_t* bytes, bool device) {
+    size_t total = 0;
+    for (auto& it : items) total += align_up(it.bytes);
+    total = std::max<size_t>(total, 256);
+    if (device) {
+        cudaError_t e = cudaMalloc(base, total);
+        if (e != cudaSuccess) {
+            ctx->err = std::string("cudaMalloc of ") + std::to_string(total) + " bytes failed: " + cudaGetErrorString(e);
+            return PASE_ERR_RESOURCE;
+        }
+    } else {
+        *base = nullptr;
+    }
+    *bytes = total;
+    char* p = (char*)*base;
+    for (auto& it : items) { *it.ptr = p; p += align_up(it.bytes); }
+    return PASE_OK;
+}
+
+// Pool 1: everything whose size the plan fixes.
+pase_status allocate(pase_ctx* ctx, bool device) {
     const Plan& P = ctx->P;
     const int n = P.n, m = P.m;
-    const int64_t nterms_total = [&] {
-        int64_t t = 0;
-        for (int i = 0; i < n; ++i) t += 1 + (int64_t)P.egt[i].size() + (int64_t)P.children[i].size();
-        return t;
-    }();
-    struct Item { void** ptr; size_t bytes; };
+    int64_t nterms_total = 0;
+    for (int i = 0; i < n; ++i) nterms_total += 1 + (int64_t)P.egt[i].size() + (int64_t)P.children[i].size();
     const int64_t ncfg = P.cfg_off[n];
+    ctx->nchunks = (int)cost_chunks(P).size();
     std::vector<Item> items = {
         {(void**)&ctx->d_nodes, sizeof(pase_node) * n},
         {(void**)&ctx->d_K, sizeof(int32_t) * n},
@@ -144,18 +167,13 @@ pase_status allocate(pase_ctx* ctx) {
         {(void**)&ctx->d_cfg, sizeof(int32_t) * pase::kMaxDims * ncfg},
         {(void**)&ctx->d_loff, sizeof(int64_t) * (n + 1)},
         {(void**)&ctx->d_edges, sizeof(EdgeDesc) * std::max(m, 1)},
-        {(void**)&ctx->d_chunks, sizeof(pase::CostChunk) * (size_t)nchunks_of(P)},
+        {(void**)&ctx->d_chunks, sizeof(pase::CostChunk) * (size_t)ctx->nchunks},
         {(void**)&ctx->d_L, sizeof(double) * P.loff[n]},
         {(void**)&ctx->d_W, sizeof(double) * std::max<int64_t>(P.woff[m], 1)},
         {(void**)&ctx->d_T, sizeof(double) * P.toff[n]},
         {(void**)&ctx->d_A, sizeof(uint16_t) * P.toff[n]},
         {(void**)&ctx->d_vd, sizeof(VertexDesc) * n},
         {(void**)&ctx->d_td, sizeof(TermDesc) * nterms_total},
-        {(void**)&ctx->d_tasks, sizeof(pase::TaskDesc) * (size_t)max_tasks_of(P, ctx->nblocks)},
-        {(void**)&ctx->d_sched, sizeof(int32_t) * (pase::kSchedLine + (size_t)n)},
-        {(void**)&ctx->d_sched_init, sizeof(int32_t) * (pase::kSchedLine + (size_t)n)},
-        {(void**)&ctx->d_order, sizeof(int32_t) * (size_t)max_tasks_of(P, ctx->nblocks)},
-        {(void**)&ctx->d_trace, trace_on() ? sizeof(int64_t) * 4 * (size_t)max_tasks_of(P, ctx->nblocks) : 0},
         {(void**)&ctx->d_bt, sizeof(pase::BtDesc) * n},
         {(void**)&ctx->d_bt_off, sizeof(int32_t) * (n + 1)},
         {(void**)&ctx->d_choice, sizeof(int32_t) * n},
@@ -172,19 +190,11 @@ pase_status allocate(pase_ctx* ctx) {
         ctx->err = buf;
         return PASE_ERR_RESOURCE;
     }
-    cudaError_t e = cudaMalloc(&ctx->pool, total);
-    if (e != cudaSuccess) {
-        ctx->err = std::string("cudaMalloc of ") + std::to_string(total) + " bytes failed: " + cudaGetErrorString(e);
-        return PASE_ERR_RESOURCE;
-    }
-    ctx->pool_bytes = total;
-    char* p = (char*)ctx->pool;
-    for (auto& it : items) { *it.ptr = p; p += align_up(it.bytes); }
-    return PASE_OK;
+    return carve(ctx, items, &ctx->pool, &ctx->pool_bytes, device);
 }
 
-// Build vertex/term descriptors (DESIGN §4 layout) and upload all static inputs.
-pase_status upload(pase_ctx* ctx) {
+// Vertex/term descriptors, the task schedule (schedule.cpp), pool 2, upload.
+pase_status prepare(pase_ctx* ctx, bool device) {
     const Plan& P = ctx->P;
     const int n = P.n, m = P.m;
     std::vector<EdgeDesc> ed(std::max(m, 1));
@@ -198,7 +208,7 @@ pase_status upload(pase_ctx* ctx) {
         d.woff = P.woff[e];
     }
     const std::vector<pase::CostChunk> chunks = cost_chunks(P);
-    ctx->nchunks = (int)chunks.size();
+    const uint64_t redundant_below = ctx->mach.redundant_below_bytes;
 
     ctx->vd.assign(n, VertexDesc{});
     ctx->td.clear();
@@ -212,27 +222,25 @@ pase_status upload(pase_ctx* ctx) {
         for (int q = 0; q < pase::kMaxDep; ++q) d.radix[q] = q < d.m ? P.K[P.dep[i][q]] : 1;
         d.T = ctx->d_T + P.toff[i];
         d.A = ctx->d_A + P.toff[i];
+        d.parent = P.parent[i];
         auto pos_of = [&](int node) {
             for (int q = 0; q < d.m; ++q) if (P.dep[i][q] == node) return q;
             return -1;
         };
         TermDesc t{};
-        // term 0: L_{sigma_i}[C]
-        t.base = ctx->d_L + P.loff[v];
+        t.base = ctx->d_L + P.loff[v];                    // term 0: L_{sigma_i}[C]
         ctx->td.push_back(t);
-        // edges to later neighbours, canonical order: row = config of the other endpoint
-        for (int e : P.egt[i]) {
+        for (int e : P.egt[i]) {                          // edges to later neighbours (E> order)
             TermDesc te{};
             const int other = P.edges[e].src == v ? P.edges[e].dst : P.edges[e].src;
             const int q = pos_of(other);
             if (q < 0) { ctx->err = "internal: E>(sigma_i) endpoint outside D(i)"; return PASE_ERR_STATE; }
-            te.base = ctx->d_W + P.woff[e];
+            te.base = ctx->d_W + P.woff[e];               // row = config of the other endpoint
             te.stride[q] = d.K;
             ctx->td.push_back(te);
         }
-        // children ascending rank: T_j coordinates (sigma_i, w_1, ...) with sigma_i fastest
-        for (int j : P.children[i]) {
-            TermDesc tc{};
+        for (int j : P.children[i]) {                     // children, ascending rank
+            TermDesc tc{};                                // T_j coords (sigma_i, w_1, ...), sigma_i fastest
             tc.base = ctx->d_T + P.toff[j];
             int64_t st = P.K[v];
             for (size_t a = 1; a < P.dep[j].size(); ++a) {
@@ -244,121 +252,74 @@ pase_status upload(pase_ctx* ctx) {
             ctx->td.push_back(tc);
         }
         d.nterms = (int32_t)ctx->td.size() - d.term0;
-        // tiled schedule: qstar = the coordinate whose first term is latest
-        // in the canonical order (longest hoistable prefix); ties -> larger radix, lower q.
-        {
-            const TermDesc* tv = ctx->td.data() + d.term0;
-            d.qstar = -1;
-            d.tstar = d.nterms;
-            int best_first = -1;
-            for (int q = 0; q < d.m; ++q) {
-                int first = -1;
-                for (int t = 0; t < d.nterms && first < 0; ++t)
-                    if (tv[t].stride[q] != 0) first = t;
-                if (first < 1) { ctx->err = "internal: D(i) coordinate not used by any term"; return PASE_ERR_STATE; }
-                if (first > best_first || (first == best_first && d.radix[q] > d.radix[d.qstar])) {
-                    best_first = first;
-                    d.qstar = q;
-                }
+        // multi-GPU partition by the top coordinate: big tables only
+        const int top = d.m - 1;
+        d.part = (ctx->world > 1 && d.m >= 2 && (uint64_t)d.nout * 8ull >= redundant_below &&
+                  d.radix[top] >= 2) ? 1 : 0;
+        // qstar = the coordinate whose first term is latest in the canonical order (longest
+        // hoistable prefix); ties -> larger radix, lower q; never the partition coordinate.
+        const TermDesc* tv = ctx->td.data() + d.term0;
+        d.qstar = -1;
+        d.tstar = d.nterms;
+        int best_first = -1;
+        for (int q = 0; q < d.m; ++q) {
+            int first = -1;
+            for (int t = 0; t < d.nterms && first < 0; ++t)
+                if (tv[t].stride[q] != 0) first = t;
+            if (first < 1) { ctx->err = "internal: D(i) coordinate not used by any term"; return PASE_ERR_STATE; }
+            if (d.part && q == top) continue;
+            if (first > best_first || (first == best_first && d.radix[q] > d.radix[d.qstar])) {
+                best_first = first;
+                d.qstar = q;
             }
-            if (d.qstar >= 0) d.tstar = best_first;
-            d.rq = d.qstar >= 0 ? d.radix[d.qstar] : 1;
-            d.ntile = (d.rq + pase::kTile - 1) / pase::kTile;
-            d.ostride_q = 1;
-            for (int q = 0; q < d.qstar; ++q) d.ostride_q *= d.radix[q];
-            if (d.qstar < 0) d.ostride_q = 0;
-            d.ncombo = d.nout / d.rq;
-            d.nitems = d.ncombo * d.ntile;
-            bool wide = d.nitems >= (int64_t(1) << 31);              // 32-bit item decode
-            for (int t = 0; t < d.nterms; ++t)
-                for (int q = 0; q < d.m; ++q)
-                    if (tv[t].stride[q] >= (int64_t(1) << 31) / 16) wide = true;
-            const int NP = d.tstar, NS = d.nterms - d.tstar;
-            if (!wide && NP >= 1 && NP <= 4 && NS >= 0 && NS <= 3) {
-                d.glog = lane_group_log2(d.K);
-                d.shape = (NP - 1) * 16 + NS * 4 + (d.glog - 2);
-            } else {                                                 // generic kernel
-                d.glog = d.K <= 4 ? 2 : d.K <= 8 ? 3 : d.K <= 16 ? 4 : 5;
-                d.shape = -1;
-            }
-            // persistent tasks: one item per lane group of a CTA for small vertices (latency),
-            // about kTasksPerBlock tasks per CTA of the grid for the big ones (balance)
-            const int64_t units = d.shape >= 0 ? d.nitems : d.nout;
-            const int64_t groups = 256 >> d.glog;
-            const int64_t spread = (int64_t)kTasksPerBlock * std::max(ctx->nblocks, 1);
-            int64_t ti = std::max<int64_t>(groups, (units + spread - 1) / spread);
-            ti = (ti + groups - 1) / groups * groups;
-            d.ntasks = (int32_t)((units + ti - 1) / ti);
-            d.items_per_task = (int32_t)std::min<int64_t>(ti, INT32_MAX);
-            d.parent = P.parent[i];
+        }
+        if (d.qstar >= 0) d.tstar = best_first;
+        d.rq = d.qstar >= 0 ? d.radix[d.qstar] : 1;
+        d.ntile = (d.rq + pase::kTile - 1) / pase::kTile;
+        d.ostride_q = 1;
+        for (int q = 0; q < d.qstar; ++q) d.ostride_q *= d.radix[q];
+        if (d.qstar < 0) d.ostride_q = 0;
+        d.ncombo = d.nout / d.rq;
+        d.nitems = d.ncombo * d.ntile;
+        bool wide = d.nitems >= (int64_t(1) << 31);       // 32-bit item decode
+        for (int t = 0; t < d.nterms; ++t)
+            for (int q = 0; q < d.m; ++q)
+                if (tv[t].stride[q] >= (int64_t(1) << 31) / 16) wide = true;
+        const int NP = d.tstar, NS = d.nterms - d.tstar;
+        if (!wide && NP >= 1 && NP <= 4 && NS >= 0 && NS <= 3) {
+            d.glog = lane_group_log2(d.K);
+            d.shape = (NP - 1) * 16 + NS * 4 + (d.glog - 2);
+        } else {                                          // generic kernel
+            d.glog = d.K <= 4 ? 2 : d.K <= 8 ? 3 : d.K <= 16 ? 4 : 5;
+            d.shape = -1;
         }
     }
-    // persistent schedule: tasks in rank order (a topological order of the tree)
-    std::vector<pase::TaskDesc> tasks;
-    for (int i = 0; i < n; ++i) {
-        VertexDesc& d = ctx->vd[i];
-        const int64_t units = d.shape >= 0 ? d.nitems : d.nout, ti = d.items_per_task;
-        d.task0 = (int32_t)tasks.size();
-        for (int64_t a = 0; a < units; a += ti) tasks.push_back({i, 0, a, std::min(units, a + ti)});
-        if ((int64_t)tasks.size() - d.task0 != d.ntasks) { ctx->err = "internal: task count"; return PASE_ERR_STATE; }
-    }
-    if ((int64_t)tasks.size() > max_tasks_of(P, ctx->nblocks)) { ctx->err = "internal: task bound"; return PASE_ERR_STATE; }
-    ctx->ntasks = (int)tasks.size();
-    // Static claim order: list-schedule the task DAG on nblocks simulated CTAs, ready tasks
-    // by decreasing bottom level (longest estimated path to the root), i.e. critical path
-    // first.  Estimated task time: ~3 us of dependent-latency overhead + candidates at
-    // ~3e9 candidates/s per CTA.
-    const int64_t ntk = (int64_t)tasks.size();
-    std::vector<double> tdur(ntk), bl(n, 0.0);
-    for (int64_t t = 0; t < ntk; ++t) {
-        const VertexDesc& d = ctx->vd[tasks[t].vtx];
-        const double cand = (double)(tasks[t].i1 - tasks[t].i0) * d.K * (d.shape >= 0 ? pase::kTile : 1);
-        tdur[t] = 3.0 + cand / 3000.0;
-    }
-    for (int i = n - 1; i >= 0; --i) {              // parents have higher ranks
-        const VertexDesc& d = ctx->vd[i];
-        const double vt = std::max(tdur[d.task0], (double)d.ntasks * tdur[d.task0] / std::max(ctx->nblocks, 1));
-        bl[i] = vt + (P.parent[i] >= 0 ? bl[P.parent[i]] : 0.0);
-    }
-    std::vector<int32_t> order;
-    order.reserve(ntk);
-    {
-        std::vector<int64_t> pend(n, 0);
-        for (int i = 0; i < n; ++i)
-            for (int j : P.children[i]) pend[i] += ctx->vd[j].ntasks;
-        using RT = std::pair<double, int32_t>;                         // (priority, -task)
-        std::priority_queue<RT> ready;
-        using EV = std::pair<double, int32_t>;                         // (finish time, task)
-        std::priority_queue<EV, std::vector<EV>, std::greater<EV>> events;
-        auto release = [&](int v) {
-            for (int k = 0; k < ctx->vd[v].ntasks; ++k) ready.push({bl[v], -(ctx->vd[v].task0 + k)});
-        };
-        for (int i = 0; i < n; ++i)
-            if (P.children[i].empty()) release(i);
-        int free_w = std::max(ctx->nblocks, 1);
-        double now = 0.0;
-        while ((int64_t)order.size() < ntk) {
-            while (free_w > 0 && !ready.empty()) {
-                const int32_t t = -ready.top().second;
-                ready.pop();
-                order.push_back(t);
-                --free_w;
-                events.push({now + tdur[t], t});
-            }
-            if (events.empty()) { ctx->err = "internal: task DAG is not schedulable"; return PASE_ERR_STATE; }
-            const EV e = events.top();
-            events.pop();
-            now = e.first;
-            ++free_w;
-            const int par = P.parent[tasks[e.second].vtx];
-            if (par >= 0 && --pend[par] == 0) release(par);
-        }
-    }
-    // scheduler state at solve start: [claim counter | pending[n]]
-    std::vector<int32_t> sched(pase::kSchedLine + (size_t)n, 0);
-    for (int i = 0; i < n; ++i)
-        for (int j : P.children[i]) sched[pase::kSchedLine + i] += ctx->vd[j].ntasks;
-    ctx->sched_bytes = sizeof(int32_t) * sched.size();
+    // tasks, broadcast flags, pending counters, claim order (schedule.cpp)
+    pase_status st = pase::build_schedule(P, ctx->vd, ctx->world, ctx->rank, ctx->nblocks, ctx->sp, ctx->err);
+    if (st) return st;
+    ctx->ntasks = (int)ctx->sp.tasks.size();
+    ctx->total_tasks = ctx->sp.total_tasks;
+    for (VertexDesc& d : ctx->vd) d.npeer = d.bcast ? ctx->world - 1 : 0;
+    // pool 2
+    const size_t sched_words = pase::kSchedLine + (size_t)n;
+    ctx->sched_bytes = sizeof(int32_t) * sched_words;
+    std::vector<Item> items2 = {
+        {(void**)&ctx->d_sched, ctx->sched_bytes},
+        {(void**)&ctx->d_sched_init, ctx->sched_bytes},
+        {(void**)&ctx->d_bar, sizeof(int32_t) * 3 * pase::kSchedLine},
+        {(void**)&ctx->d_tasks, sizeof(pase::TaskDesc) * std::max<size_t>(ctx->sp.tasks.size(), 1)},
+        {(void**)&ctx->d_order, sizeof(int32_t) * std::max<size_t>(ctx->sp.order.size(), 1)},
+        {(void**)&ctx->d_trace, trace_on() ? sizeof(int64_t) * 4 * std::max<size_t>(ctx->sp.tasks.size(), 1) : 0},
+    };
+    if ((st = carve(ctx, items2, &ctx->pool2, &ctx->pool2_bytes, device))) return st;
+    std::vector<int32_t> sched(sched_words, 0);
+    for (int i = 0; i < n; ++i) sched[pase::kSchedLine + i] = ctx->sp.pending[i];
+    // single-rank peer table (connect() fills the group's)
+    ctx->peers = pase::Peers{};
+    ctx->peers.world = ctx->world;
+    ctx->peers.rank = ctx->rank;
+    ctx->peers.pending[ctx->rank] = ctx->d_sched + pase::kSchedLine;
+    ctx->peers.bar[ctx->rank] = ctx->d_bar;
     // back-substitution levels: lev(root) = 0, lev(i) = 1 + max lev over D(i)
     std::vector<int> blev(n, 0);
     int nlev = 0;
@@ -384,12 +345,14 @@ pase_status upload(pase_ctx* ctx) {
         }
     }
     ctx->nbtlev = nlev;
-    cudaStream_t s = ctx->stream;
     ctx->h2d_bytes = sizeof(pase_node) * n + sizeof(int32_t) * n + sizeof(int64_t) * (n + 1) * 2 +
                      sizeof(int32_t) * P.cfg.size() + sizeof(EdgeDesc) * ed.size() +
-                     sizeof(pase::CostChunk) * chunks.size() + sizeof(VertexDesc) * n + sizeof(TermDesc) * ctx->td.size() +
-                     sizeof(pase::BtDesc) * n + sizeof(int32_t) * (nlev + 1) +
-                     sizeof(pase::TaskDesc) * tasks.size() + ctx->sched_bytes + sizeof(int32_t) * order.size();
+                     sizeof(pase::CostChunk) * chunks.size() + sizeof(VertexDesc) * n +
+                     sizeof(TermDesc) * ctx->td.size() + sizeof(pase::BtDesc) * n + sizeof(int32_t) * (nlev + 1) +
+                     sizeof(pase::TaskDesc) * ctx->sp.tasks.size() + ctx->sched_bytes +
+                     sizeof(int32_t) * ctx->sp.order.size();
+    if (!device) return PASE_OK;
+    cudaStream_t s = ctx->stream;
     CUDA_TRY(cudaMemcpyAsync(ctx->d_nodes, P.nodes.data(), sizeof(pase_node) * n, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_K, P.K.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_cfg_off, P.cfg_off.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
@@ -399,17 +362,19 @@ pase_status upload(pase_ctx* ctx) {
     CUDA_TRY(cudaMemcpyAsync(ctx->d_chunks, chunks.data(), sizeof(pase::CostChunk) * chunks.size(), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_vd, ctx->vd.data(), sizeof(VertexDesc) * n, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_td, ctx->td.data(), sizeof(TermDesc) * ctx->td.size(), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_tasks, tasks.data(), sizeof(pase::TaskDesc) * tasks.size(), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_tasks, ctx->sp.tasks.data(), sizeof(pase::TaskDesc) * ctx->sp.tasks.size(), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_order, ctx->sp.order.data(), sizeof(int32_t) * ctx->sp.order.size(), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_sched_init, sched.data(), ctx->sched_bytes, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_order, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(ctx->d_bar, 0, sizeof(int32_t) * 3 * pase::kSchedLine, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_bt, bt.data(), sizeof(pase::BtDesc) * n, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_bt_off, bt_off.data(), sizeof(int32_t) * (nlev + 1), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaStreamSynchronize(s));   // host vectors above are stack-local
     return PASE_OK;
 }
 
-// Record the whole solve as one CUDA graph.  DP kernels are issued in rank order; a vertex
-// waits on its children's events only, so independent subtrees overlap.
+// Issue (or capture) the whole solve.  Persistent schedule: cost tables -> reset scheduler
+// -> [group barrier] -> dp_persistent -> [group barrier] -> back-substitution -> D2H.
+// PASE_SCHEDULE=launches: one kernel per vertex, children -> parent event edges.
 pase_status issue_schedule(pase_ctx* ctx, bool capture) {
     const Plan& P = ctx->P;
     const int n = P.n;
@@ -419,7 +384,7 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
         ctx->aux.resize(nstreams);
         for (auto& s : ctx->aux) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     }
-    std::vector<cudaEvent_t> done(n);
+    std::vector<cudaEvent_t> done(ctx->persistent ? 0 : n);
     for (auto& e : done) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     cudaEvent_t start;
     CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
@@ -428,43 +393,45 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
     cudaStream_t s = ctx->stream;
     if (capture) CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     const unsigned ext = capture ? cudaEventRecordExternal : cudaEventRecordDefault;
+    int32_t* d_err = ctx->d_bar + 2 * pase::kSchedLine;
+    CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int32_t), s));
     if (!ctx->override_tables)
         pase::launch_cost_tables(ctx->d_nodes, ctx->d_K, ctx->d_cfg_off, ctx->d_cfg, ctx->d_loff, n,
-                                 ctx->d_edges, ctx->d_chunks, ctx->nchunks, P.r, ctx->d_L,
-                                 ctx->d_W, s);
+                                 ctx->d_edges, ctx->d_chunks, ctx->nchunks, P.r, ctx->d_L, ctx->d_W, s);
     // phase split: external event nodes (plain records would only become capture edges)
     CUDA_TRY(cudaEventRecordWithFlags(ctx->ev_mid, s, ext));
     std::vector<char> used(nstreams, 0);
     if (ctx->persistent) {
         CUDA_TRY(cudaMemcpyAsync(ctx->d_sched, ctx->d_sched_init, ctx->sched_bytes, cudaMemcpyDeviceToDevice, s));
+        if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, s);
         pase::launch_dp_persistent(ctx->d_vd, ctx->d_td, ctx->d_tasks, ctx->d_order, ctx->ntasks, ctx->d_sched,
-                                   ctx->nblocks,
-                                   trace_on() ? ctx->d_trace : nullptr, s);
+                                   d_err, ctx->peers, ctx->nblocks, trace_on() ? ctx->d_trace : nullptr, s);
+        if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, s);
     } else {
-    CUDA_TRY(cudaEventRecord(start, s));
-    // assign each vertex the stream of its first child (chains stay on one stream)
-    std::vector<int> sid(n, -1);
-    int rr = 0;
-    for (int i = 0; i < n; ++i) {
-        sid[i] = P.children[i].empty() ? (rr++ % nstreams) : sid[P.children[i][0]];
-        cudaStream_t si = ctx->aux[sid[i]];
-        if (!used[sid[i]]) { CUDA_TRY(cudaStreamWaitEvent(si, start, 0)); used[sid[i]] = 1; }
-        for (int j : P.children[i])
-            if (sid[j] != sid[i]) CUDA_TRY(cudaStreamWaitEvent(si, done[j], 0));
-        pase::launch_dp_vertex(ctx->d_vd, ctx->d_td, i, ctx->vd[i], si);
-        CUDA_TRY(cudaEventRecord(done[i], si));
-    }
-    for (int k = 0; k < nstreams; ++k)
-        if (used[k]) {
-            CUDA_TRY(cudaEventRecord(join[k], ctx->aux[k]));
-            CUDA_TRY(cudaStreamWaitEvent(s, join[k], 0));
+        CUDA_TRY(cudaEventRecord(start, s));
+        std::vector<int> sid(n, -1);                      // a chain stays on one stream
+        int rr = 0;
+        for (int i = 0; i < n; ++i) {
+            sid[i] = P.children[i].empty() ? (rr++ % nstreams) : sid[P.children[i][0]];
+            cudaStream_t si = ctx->aux[sid[i]];
+            if (!used[sid[i]]) { CUDA_TRY(cudaStreamWaitEvent(si, start, 0)); used[sid[i]] = 1; }
+            for (int j : P.children[i])
+                if (sid[j] != sid[i]) CUDA_TRY(cudaStreamWaitEvent(si, done[j], 0));
+            pase::launch_dp_vertex(ctx->d_vd, ctx->d_td, i, ctx->vd[i], si);
+            CUDA_TRY(cudaEventRecord(done[i], si));
         }
+        for (int k = 0; k < nstreams; ++k)
+            if (used[k]) {
+                CUDA_TRY(cudaEventRecord(join[k], ctx->aux[k]));
+                CUDA_TRY(cudaStreamWaitEvent(s, join[k], 0));
+            }
     }
     CUDA_TRY(cudaEventRecordWithFlags(ctx->ev_dp, s, ext));
     pase::launch_backtrack(ctx->d_bt, ctx->d_bt_off, ctx->nbtlev, n, ctx->vd[n - 1].T, ctx->d_choice,
                            ctx->d_total, s);
     CUDA_TRY(cudaMemcpyAsync(ctx->h_choice, ctx->d_choice, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(ctx->h_total, ctx->d_total, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_err, d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     cudaError_t ce = cudaSuccess;
     cudaGraph_t graph = nullptr;
     if (capture) ce = cudaStreamEndCapture(s, &graph);
@@ -480,13 +447,14 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
     return PASE_OK;
 }
 
-// The solve schedule is recorded once as a CUDA graph; PASE_NO_GRAPH=1 issues it directly
-// on the streams at every solve instead (profiling: kernels then launch in rank order).
+// The solve schedule is recorded once as a CUDA graph (multi-GPU: after pase_connect);
+// PASE_NO_GRAPH=1 issues it directly at every solve instead (kernels then launch in order).
 pase_status record_graph(pase_ctx* ctx) {
-    ctx->stats.n_launches = (ctx->override_tables ? 0 : 1) + (ctx->persistent ? 1 : ctx->P.n) + 1;
+    const int dp_launches = ctx->persistent ? 1 + (ctx->world > 1 ? 2 : 0) : ctx->P.n;
+    ctx->stats.n_launches = (ctx->override_tables ? 0 : 1) + dp_launches + 1;
     const char* ng = std::getenv("PASE_NO_GRAPH");
     ctx->no_graph = ng && ng[0] == '1';
-    if (ctx->no_graph) return PASE_OK;
+    if (ctx->no_graph || (ctx->world > 1 && !ctx->connected)) return PASE_OK;
     return issue_schedule(ctx, true);
 }
 
@@ -503,7 +471,7 @@ void fill_stats(pase_ctx* ctx) {
     s.cost_entries = (uint64_t)(P.loff[P.n] + P.woff[P.m]);
     // each table written once (8 B value + 2 B argmin) and read once by its parent;
     // W_e rows and L read by the vertex that owns them.
-    uint64_t b = 0, ops = 0;
+    uint64_t b = 0, ops = 0, comm = 0;
     for (int i = 0; i < P.n; ++i) {
         const int v = P.sigma[i];
         const uint64_t terms = 1 + P.egt[i].size() + P.children[i].size();
@@ -512,14 +480,32 @@ void fill_stats(pase_ctx* ctx) {
         for (int j : P.children[i]) b += (uint64_t)P.tsize[j] * 8u;
         for (int e : P.egt[i]) b += 8ull * (uint64_t)P.K[P.edges[e].src] * (uint64_t)P.K[P.edges[e].dst];
         b += 8ull * (uint64_t)P.K[v];
+        if (i < (int)ctx->vd.size() && ctx->vd[i].bcast) {   // peer bytes this rank writes
+            const uint64_t mine = (uint64_t)P.tsize[i] / std::max(ctx->world, 1);
+            comm += mine * ((ctx->vd[i].bcast & 1 ? 8u : 0u) + 2u) * (uint64_t)(ctx->world - 1);
+        }
     }
     s.alg_bytes_dp = b;
     s.dp_fp64_ops = ops;
     s.alg_bytes_tables = 8ull * s.cost_entries;
-    s.comm_bytes = 0;
+    s.comm_bytes = comm;
     s.h2d_bytes = ctx->h2d_bytes;
-    s.d2h_bytes = sizeof(int32_t) * P.n + sizeof(double);
+    s.d2h_bytes = sizeof(int32_t) * P.n + sizeof(double) + sizeof(int32_t);
 }
+
+// Group handle blob (PASE_HANDLE_BYTES): how a peer reaches this context's pools.
+struct HandleBlob {
+    uint32_t magic;
+    int32_t version;
+    int64_t pid;
+    int32_t device, world, rank, n;
+    int64_t total_tasks;
+    cudaIpcMemHandle_t h1, h2;
+    uint64_t raw1, raw2;
+    uint64_t off_T, off_A, off_pending, off_bar;
+};
+static_assert(sizeof(HandleBlob) <= PASE_HANDLE_BYTES, "handle blob too large");
+constexpr uint32_t kMagic = 0x50415345;   // "PASE"
 
 }  // namespace
 
@@ -533,20 +519,31 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
     if (!ctx) { g_create_err = "out of host memory"; return PASE_ERR_RESOURCE; }
     if (!m) { g_create_err = "machine is NULL"; delete ctx; return PASE_ERR_INVALID; }
     ctx->mach = *m;
-    if (m->world > 1) {
-        g_create_err = "multi-GPU contexts (world > 1) are not supported by this build";
+    ctx->world = std::max(1, m->world);
+    ctx->rank = m->rank;
+    ctx->virtual_ranks = m->virtual_ranks != 0;
+    if (ctx->world > pase::kMaxWorld || ctx->rank < 0 || ctx->rank >= ctx->world) {
+        g_create_err = "world must be in [1, 8] and 0 <= rank < world";
         delete ctx;
         return PASE_ERR_INVALID;
     }
-    pase_status st = pase::build_plan(g, p, m, ctx->P, ctx->err);
+    ctx->dev = m->cuda_device;
     auto fail = [&](pase_status code) {
         g_create_err = ctx->err;
         pase_destroy(ctx);
         return code;
     };
+    pase_status st = pase::build_plan(g, p, m, ctx->P, ctx->err);
     if (st) return fail(st);
-    ctx->dev = m->cuda_device;
-    if (ctx->dev < 0) {                      // host-only planning context (no device work)
+    const bool device = ctx->dev >= 0;
+    {
+        const char* sc = std::getenv("PASE_SCHEDULE");
+        ctx->persistent = !(sc && std::strcmp(sc, "launches") == 0) || ctx->world > 1;
+    }
+    if (!device) {                          // host-only planning context (no device work)
+        ctx->nblocks = std::max(1, 2 * 148 / (ctx->virtual_ranks ? ctx->world : 1));
+        if ((st = allocate(ctx, false))) return fail(st);
+        if ((st = prepare(ctx, false))) return fail(st);
         fill_stats(ctx);
         ctx->stats.n_launches = 0;
         ctx->stats.ms_create =
@@ -568,7 +565,8 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
         ctx->own_stream = true;
     }
     if (cudaMallocHost(&ctx->h_choice, sizeof(int32_t) * ctx->P.n) != cudaSuccess ||
-        cudaMallocHost(&ctx->h_total, sizeof(double)) != cudaSuccess) {
+        cudaMallocHost(&ctx->h_total, sizeof(double)) != cudaSuccess ||
+        cudaMallocHost(&ctx->h_err, sizeof(int32_t)) != cudaSuccess) {
         ctx->err = "cudaMallocHost failed";
         return fail(PASE_ERR_CUDA);
     }
@@ -578,19 +576,20 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
         return fail(PASE_ERR_CUDA);
     }
     {
-        const char* sc = std::getenv("PASE_SCHEDULE");
-        ctx->persistent = !(sc && std::strcmp(sc, "launches") == 0);
         int sms = 0;
         if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev) != cudaSuccess || sms < 1) {
             ctx->err = "cudaDeviceGetAttribute(MultiProcessorCount) failed";
             return fail(PASE_ERR_CUDA);
         }
-        ctx->nblocks = std::max(1, pase::persistent_blocks_per_sm()) * sms;
+        // virtual ranks share one device: each persistent grid gets 1/world of its CTA slots,
+        // so all ranks' grids are co-resident (they wait on each other)
+        ctx->nblocks = std::max(1, std::max(1, pase::persistent_blocks_per_sm()) * sms /
+                                       (ctx->virtual_ranks ? ctx->world : 1));
     }
     auto t_plan = std::chrono::steady_clock::now();
-    if ((st = allocate(ctx))) return fail(st);
+    if ((st = allocate(ctx, true))) return fail(st);
     auto t_alloc = std::chrono::steady_clock::now();
-    if ((st = upload(ctx))) return fail(st);
+    if ((st = prepare(ctx, true))) return fail(st);
     auto t_upload = std::chrono::steady_clock::now();
     if ((st = record_graph(ctx))) return fail(st);
     auto t_graph = std::chrono::steady_clock::now();
@@ -605,9 +604,12 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
     return PASE_OK;
 }
 
-pase_status pase_solve(pase_ctx* ctx, int32_t* configs_out, int32_t* config_index_out, double* total_cost_out) {
+pase_status pase_launch(pase_ctx* ctx) {
     if (!ctx) return PASE_ERR_INVALID;
-    if (!ctx->exec && !ctx->no_graph) { ctx->err = "context has no solve schedule (host-only planning context?)"; return PASE_ERR_STATE; }
+    if (ctx->dev < 0) { ctx->err = "host-only planning context: no solve"; return PASE_ERR_STATE; }
+    if (ctx->world > 1 && !ctx->connected) { ctx->err = "multi-GPU context: call pase_connect first"; return PASE_ERR_STATE; }
+    if (!ctx->exec && !ctx->no_graph) { ctx->err = "context has no solve schedule"; return PASE_ERR_STATE; }
+    if (ctx->launched) { ctx->err = "pase_launch called twice without pase_finish"; return PASE_ERR_STATE; }
     CUDA_TRY(cudaSetDevice(ctx->dev));
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
     if (ctx->no_graph) {
@@ -617,7 +619,21 @@ pase_status pase_solve(pase_ctx* ctx, int32_t* configs_out, int32_t* config_inde
         CUDA_TRY(cudaGraphLaunch(ctx->exec, ctx->stream));
     }
     CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->launched = true;
+    return PASE_OK;
+}
+
+pase_status pase_finish(pase_ctx* ctx, int32_t* configs_out, int32_t* config_index_out, double* total_cost_out) {
+    if (!ctx) return PASE_ERR_INVALID;
+    if (!ctx->launched) { ctx->err = "pase_finish without pase_launch"; return PASE_ERR_STATE; }
+    ctx->launched = false;
+    CUDA_TRY(cudaSetDevice(ctx->dev));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (*ctx->h_err) {
+        ctx->err = std::string("scheduler wait timed out (code ") + std::to_string(*ctx->h_err) +
+                   "): ranks of the group not running concurrently?";
+        return PASE_ERR_STATE;
+    }
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     ctx->stats.ms_solve = ms;
@@ -639,6 +655,118 @@ pase_status pase_solve(pase_ctx* ctx, int32_t* configs_out, int32_t* config_inde
     return PASE_OK;
 }
 
+pase_status pase_solve(pase_ctx* ctx, int32_t* configs_out, int32_t* config_index_out, double* total_cost_out) {
+    pase_status st = pase_launch(ctx);
+    if (st) return st;
+    return pase_finish(ctx, configs_out, config_index_out, total_cost_out);
+}
+
+pase_status pase_export_handle(const pase_ctx* ctx_c, void* blob) {
+    pase_ctx* ctx = const_cast<pase_ctx*>(ctx_c);
+    if (!ctx || !blob) return PASE_ERR_INVALID;
+    if (ctx->dev < 0) { ctx->err = "host-only planning context has no device memory"; return PASE_ERR_STATE; }
+    HandleBlob h{};
+    h.magic = kMagic;
+    h.version = 1;
+    h.pid = (int64_t)getpid();
+    h.device = ctx->dev;
+    h.world = ctx->world;
+    h.rank = ctx->rank;
+    h.n = ctx->P.n;
+    h.total_tasks = ctx->total_tasks;
+    CUDA_TRY(cudaSetDevice(ctx->dev));
+    CUDA_TRY(cudaIpcGetMemHandle(&h.h1, ctx->pool));
+    CUDA_TRY(cudaIpcGetMemHandle(&h.h2, ctx->pool2));
+    h.raw1 = (uint64_t)(uintptr_t)ctx->pool;
+    h.raw2 = (uint64_t)(uintptr_t)ctx->pool2;
+    h.off_T = (uint64_t)((char*)ctx->d_T - (char*)ctx->pool);
+    h.off_A = (uint64_t)((char*)ctx->d_A - (char*)ctx->pool);
+    h.off_pending = (uint64_t)((char*)(ctx->d_sched + pase::kSchedLine) - (char*)ctx->pool2);
+    h.off_bar = (uint64_t)((char*)ctx->d_bar - (char*)ctx->pool2);
+    std::memset(blob, 0, PASE_HANDLE_BYTES);
+    std::memcpy(blob, &h, sizeof h);
+    return PASE_OK;
+}
+
+pase_status pase_connect(pase_ctx* ctx, const void* blobs) {
+    if (!ctx || !blobs) return PASE_ERR_INVALID;
+    if (ctx->dev < 0) { ctx->err = "host-only planning context cannot connect"; return PASE_ERR_STATE; }
+    if (ctx->connected) { ctx->err = "already connected"; return PASE_ERR_STATE; }
+    CUDA_TRY(cudaSetDevice(ctx->dev));
+    std::vector<double*> Tb(ctx->world);
+    std::vector<uint16_t*> Ab(ctx->world);
+    for (int q = 0; q < ctx->world; ++q) {
+        HandleBlob h;
+        std::memcpy(&h, (const char*)blobs + (size_t)q * PASE_HANDLE_BYTES, sizeof h);
+        if (h.magic != kMagic || h.world != ctx->world || h.rank != q || h.n != ctx->P.n ||
+            h.total_tasks != ctx->total_tasks) {
+            ctx->err = "pase_connect: handle " + std::to_string(q) + " does not belong to this group / plan";
+            return PASE_ERR_INVALID;
+        }
+        char *b1, *b2;
+        if (q == ctx->rank) {
+            b1 = (char*)ctx->pool;
+            b2 = (char*)ctx->pool2;
+        } else if (h.pid == (int64_t)getpid()) {        // virtual ranks in one process
+            b1 = (char*)(uintptr_t)h.raw1;
+            b2 = (char*)(uintptr_t)h.raw2;
+            if (h.device != ctx->dev) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(h.device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+                    ctx->err = std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e);
+                    return PASE_ERR_CUDA;
+                }
+                cudaGetLastError();
+            }
+        } else {                                        // another process: IPC over NVLink
+            void *p1 = nullptr, *p2 = nullptr;
+            CUDA_TRY(cudaIpcOpenMemHandle(&p1, h.h1, cudaIpcMemLazyEnablePeerAccess));
+            ctx->ipc_opened.push_back(p1);
+            CUDA_TRY(cudaIpcOpenMemHandle(&p2, h.h2, cudaIpcMemLazyEnablePeerAccess));
+            ctx->ipc_opened.push_back(p2);
+            b1 = (char*)p1;
+            b2 = (char*)p2;
+        }
+        Tb[q] = (double*)(b1 + h.off_T);
+        Ab[q] = (uint16_t*)(b1 + h.off_A);
+        ctx->peers.pending[q] = (int32_t*)(b2 + h.off_pending);
+        ctx->peers.bar[q] = (int32_t*)(b2 + h.off_bar);
+    }
+    for (int i = 0; i < ctx->P.n; ++i) {
+        VertexDesc& d = ctx->vd[i];
+        int k = 0;
+        for (int q = 0; q < ctx->world; ++q) {
+            if (q == ctx->rank) continue;
+            d.Tpeer[k] = Tb[q] + ctx->P.toff[i];
+            d.Apeer[k] = Ab[q] + ctx->P.toff[i];
+            ++k;
+        }
+    }
+    CUDA_TRY(cudaMemcpy(ctx->d_vd, ctx->vd.data(), sizeof(VertexDesc) * ctx->P.n, cudaMemcpyHostToDevice));
+    ctx->connected = true;
+    return record_graph(ctx);
+}
+
+int64_t pase_get_schedule(const pase_ctx* ctx, int32_t* vinfo, int64_t* tasks, int32_t* order) {
+    if (!ctx) return -1;
+    const int n = ctx->P.n;
+    if (vinfo)
+        for (int i = 0; i < n; ++i) {
+            vinfo[4 * i + 0] = ctx->vd[i].part;
+            vinfo[4 * i + 1] = ctx->vd[i].bcast;
+            vinfo[4 * i + 2] = ctx->vd[i].ntasks;
+            vinfo[4 * i + 3] = ctx->sp.pending[i];
+        }
+    if (tasks)
+        for (size_t t = 0; t < ctx->sp.tasks.size(); ++t) {
+            tasks[3 * t + 0] = ctx->sp.tasks[t].vtx;
+            tasks[3 * t + 1] = ctx->sp.tasks[t].i0;
+            tasks[3 * t + 2] = ctx->sp.tasks[t].i1;
+        }
+    if (order) std::copy(ctx->sp.order.begin(), ctx->sp.order.end(), order);
+    return (int64_t)ctx->sp.tasks.size();
+}
+
 pase_status pase_get_stats(const pase_ctx* ctx, pase_stats* out) {
     if (!ctx || !out) return PASE_ERR_INVALID;
     *out = ctx->stats;
@@ -653,15 +781,19 @@ void pase_destroy(pase_ctx* ctx) {
     if (!ctx) return;
     if (ctx->dev < 0) { delete ctx; return; }
     cudaSetDevice(ctx->dev);
+    if (ctx->launched && ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
     for (auto s : ctx->aux) cudaStreamDestroy(s);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->ev_mid) cudaEventDestroy(ctx->ev_mid);
     if (ctx->ev_dp) cudaEventDestroy(ctx->ev_dp);
+    for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
     if (ctx->pool) cudaFree(ctx->pool);
+    if (ctx->pool2) cudaFree(ctx->pool2);
     if (ctx->h_choice) cudaFreeHost(ctx->h_choice);
     if (ctx->h_total) cudaFreeHost(ctx->h_total);
+    if (ctx->h_err) cudaFreeHost(ctx->h_err);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -772,11 +904,6 @@ pase_status pase_set_profiling(pase_ctx* ctx, int32_t enable) {
     if (!ctx) return PASE_ERR_INVALID;
     ctx->profiling = enable;
     return PASE_OK;
-}
-
-pase_status pase_get_unique_id(void* uid_out) {
-    (void)uid_out;
-    return PASE_ERR_STATE;   // multi-GPU not built in this configuration
 }
 
 }  // extern "C"

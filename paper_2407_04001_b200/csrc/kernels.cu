@@ -175,9 +175,22 @@ __device__ __forceinline__ double ld(const double* p) {
     asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
     return v;
 }
-__device__ __forceinline__ void st_out(double* T, uint16_t* A, int64_t phi, double v, int c) {
-    asm volatile("st.global.f64 [%0], %1;" ::"l"(T + phi), "d"(v) : "memory");
-    asm volatile("st.global.u16 [%0], %1;" ::"l"(A + phi), "h"((unsigned short)c) : "memory");
+__device__ __forceinline__ void st_f64(double* p, double v) {
+    asm volatile("st.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_u16(uint16_t* p, int c) {
+    asm volatile("st.global.u16 [%0], %1;" ::"l"(p), "h"((unsigned short)c) : "memory");
+}
+// Output of one DP entry; multi-GPU broadcast vertices also write it into every peer's copy
+// of the table (peer stores over NVLink: the all-gather fused into the producer).
+__device__ __forceinline__ void st_out(const VertexDesc& vd, int64_t phi, double v, int c) {
+    st_f64(vd.T + phi, v);
+    st_u16(vd.A + phi, c);
+    if (vd.bcast)
+        for (int q = 0; q < vd.npeer; ++q) {
+            if (vd.bcast & 1) st_f64(vd.Tpeer[q] + phi, v);
+            st_u16(vd.Apeer[q] + phi, c);
+        }
 }
 
 // Items [first + k*stride + sub, ...) < end for the calling warp (warp-uniform loop).
@@ -278,7 +291,7 @@ __device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td
 #pragma unroll
             for (int k = 0; k < H; ++k) {
                 const int j = jbase + k;
-                if (j < nb) st_out(vd.T, vd.A, obase + (int64_t)(x0 + j) * vd.ostride_q, best[k], bestC[k]);
+                if (j < nb) st_out(vd, obase + (int64_t)(x0 + j) * vd.ostride_q, best[k], bestC[k]);
             }
         }
     }
@@ -315,7 +328,7 @@ __device__ __noinline__ void generic_items(const VertexDesc& vd, const TermDesc*
             const int oc = __shfl_xor_sync(0xffffffffu, bestC, o);
             combine(best, bestC, ob, oc);
         }
-        if (lane == 0 && K > 0) st_out(vd.T, vd.A, phi, best, bestC);
+        if (lane == 0 && K > 0) st_out(vd, phi, best, bestC);
     }
 }
 
@@ -404,13 +417,30 @@ __device__ __forceinline__ int atom_add_acq_rel(int32_t* p, int v) {
     return old;
 }
 
+__device__ __forceinline__ int ld_acquire_sys(const int32_t* p) {
+    int v;
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ld_relaxed_sys(const int32_t* p) {
+    int v;
+    asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_add_release_sys(int32_t* p, int v) {
+    asm volatile("red.release.sys.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+constexpr uint64_t kSpinTimeoutNs = 4000000000ull;    // a wait this long is reported, not hung
+
 __global__ void __launch_bounds__(256, 2)
 dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ tds,
               const TaskDesc* __restrict__ tasks, const int32_t* __restrict__ order, int ntasks,
-              int32_t* __restrict__ sched, int64_t* __restrict__ trace) {
+              int32_t* __restrict__ sched, int32_t* __restrict__ err, Peers peers,
+              int64_t* __restrict__ trace) {
     // sched: [0] claim counter (own 128-B line), [kSchedLine, +n) pending per vertex
     int32_t* head = sched;
     int32_t* pending = sched + kSchedLine;
+    const bool multi = peers.world > 1;                     // peers: .sys scope
     __shared__ VertexDesc vd;
     __shared__ TermDesc td[kMaxTermsSh];
     __shared__ int s_task;
@@ -424,7 +454,7 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
             s_task = s < ntasks ? order[s] : -1;
         }
         __syncthreads();
-        const int task = s_task;
+        int task = s_task;
         if (task < 0) break;
         const TaskDesc tk = tasks[task];
         if (tk.vtx != cur) {                                // descriptors: static, fetch now
@@ -435,21 +465,35 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
             cur = tk.vtx;
         }
         if (threadIdx.x == 0) {                             // wait for the children's tasks
-            if (ld_relaxed(pending + tk.vtx) != 0) {
+            int32_t* pv = pending + tk.vtx;
+            if ((multi ? ld_relaxed_sys(pv) : ld_relaxed(pv)) != 0) {
                 unsigned bo = 32;
-                while (ld_relaxed(pending + tk.vtx) != 0) {
+                const uint64_t t0 = globaltimer();
+                while ((multi ? ld_relaxed_sys(pv) : ld_relaxed(pv)) != 0) {
                     __nanosleep(bo);
                     bo = bo < 256 ? 2 * bo : 256;
+                    if (globaltimer() - t0 > kSpinTimeoutNs) { atomicExch(err, 1); s_task = -1; break; }
                 }
             }
-            (void)ld_acquire(pending + tk.vtx);
+            if (multi) (void)ld_acquire_sys(pv);
+            else (void)ld_acquire(pv);
             if (trace) t_start = (int64_t)globaltimer();
         }
         __syncthreads();
+        task = s_task;
+        if (task < 0) break;                                // timed out (reported via *err)
         run_shape(vd.shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1);
         __syncthreads();                                    // task's stores precede the release
         if (threadIdx.x == 0) {
-            if (vd.parent >= 0) atom_add_acq_rel(pending + vd.parent, -1);
+            if (vd.parent >= 0) {
+                if (vd.bcast & 1) {                         // every rank's copy of the parent waits
+                    for (int q = 0; q < peers.world; ++q) red_add_release_sys(peers.pending[q] + vd.parent, -1);
+                } else if (multi) {
+                    red_add_release_sys(pending + vd.parent, -1);
+                } else {
+                    atom_add_acq_rel(pending + vd.parent, -1);
+                }
+            }
             if (trace) {                                    // PASE_TRACE: per-task timeline
                 trace[4 * task + 0] = ((int64_t)smid() << 32) | (uint32_t)tk.vtx;
                 trace[4 * task + 1] = t_claim;
@@ -461,10 +505,30 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
 }
 
 void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, const TaskDesc* tasks_dev,
-                          const int32_t* order_dev, int ntasks, int32_t* sched_dev, int nblocks,
-                          int64_t* trace_dev, void* stream) {
+                          const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
+                          const Peers& peers, int nblocks, int64_t* trace_dev, void* stream) {
     dp_persistent<<<(unsigned)nblocks, 256, 0, (cudaStream_t)stream>>>(vd_dev, td_dev, tasks_dev, order_dev,
-                                                                         ntasks, sched_dev, trace_dev);
+                                                                         ntasks, sched_dev, err_dev, peers,
+                                                                         trace_dev);
+}
+
+// Group barrier between the ranks of a multi-GPU search (before and after the DP): every
+// rank adds 1 to every rank's arrival counter (release.sys, peer atomics) and waits for
+// epoch * world arrivals on its own.  bar[0] = arrivals, bar[kSchedLine] = local epoch.
+__global__ void rank_barrier(Peers peers, int32_t* bar, int32_t* err) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int e = bar[kSchedLine] + 1;
+    bar[kSchedLine] = e;
+    for (int q = 0; q < peers.world; ++q) red_add_release_sys(peers.bar[q], 1);
+    const uint64_t t0 = globaltimer();
+    while (ld_acquire_sys(bar) < e * peers.world) {
+        __nanosleep(128);
+        if (globaltimer() - t0 > kSpinTimeoutNs) { atomicExch(err, 2); break; }
+    }
+}
+
+void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev, void* stream) {
+    rank_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(peers, bar_dev, err_dev);
 }
 
 int persistent_blocks_per_sm() {

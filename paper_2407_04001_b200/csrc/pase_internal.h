@@ -73,6 +73,8 @@ struct TermDesc {            // one summand of Eq. 4 for a vertex (L, one W_e, o
     int64_t stride[kMaxDep];
 };
 
+constexpr int kMaxWorld = 8;     // search GPUs per context group (1, 2, 4, 8)
+
 struct VertexDesc {          // one DP vertex (rank i)
     int32_t K;               // |C(sigma_i)|, the reduction extent
     int32_t m;               // |D(i)|
@@ -82,7 +84,7 @@ struct VertexDesc {          // one DP vertex (rank i)
     int32_t radix[kMaxDep];  // K of each D(i) coordinate, ascending rank (lowest fastest)
     double* T;               // output table
     uint16_t* A;             // argmin table
-    // tiled schedule (DESIGN §4.2): outputs are tiled along coordinate qstar; terms
+    // tiled schedule (DESIGN §5.2): outputs are tiled along coordinate qstar; terms
     // [0, tstar) do not depend on qstar and are summed once per C per tile (hoisted prefix).
     int32_t qstar;           // tiled coordinate (-1: root, D(i) = ∅)
     int32_t tstar;           // first term depending on qstar
@@ -93,11 +95,14 @@ struct VertexDesc {          // one DP vertex (rank i)
     int64_t nitems;          // ncombo * ntile
     int32_t glog;            // log2 lane-group size
     int32_t shape;           // tiled variant (NP-1)*16 + NS*4 + (glog-2), or -1 = generic kernel
-    int32_t ntasks;          // persistent schedule: tasks of this vertex ...
-    int32_t task0;           // ... with ids [task0, task0 + ntasks)
+    int32_t ntasks;          // persistent schedule: this rank's tasks of the vertex ...
+    int32_t task0;           // ... with local ids [task0, task0 + ntasks)
     int32_t parent;          // rank of the elimination-tree parent (-1: root)
-    int32_t items_per_task;  // host-side task sizing
-    int32_t pad;
+    int32_t part;            // multi-GPU: table partitioned by its top coordinate
+    int32_t bcast;           // bit 0: write T to every rank, bit 1: write A to every rank
+    int32_t npeer;           // peers written when bcast != 0 (world - 1)
+    double* Tpeer[kMaxWorld - 1];     // this vertex's T / A in the peers' pools
+    uint16_t* Apeer[kMaxWorld - 1];
 };
 constexpr int kSchedLine = 32;   // int32 words per 128-B line (scheduler control block)
 constexpr int kMaxTermsSh = 8;   // terms staged in shared memory (tiled shapes use <= 7)
@@ -106,6 +111,26 @@ struct TaskDesc {            // persistent schedule: item range [i0, i1) of vert
     int32_t vtx, pad;
     int64_t i0, i1;
 };
+
+struct Peers {               // kernel parameter: the group's scheduler words (device pointers)
+    int32_t* pending[kMaxWorld];   // each rank's pending[n] (index = this context's rank order)
+    int32_t* bar[kMaxWorld];       // each rank's barrier counter
+    int32_t world, rank;
+};
+
+constexpr int kTasksPerBlock = 4;   // big vertices: ~4 tasks per CTA of the grid
+
+struct SchedPlan {           // build_schedule output for one rank
+    std::vector<TaskDesc> tasks;   // this rank's tasks, vertex-major (VertexDesc.task0)
+    std::vector<int32_t> order;    // claim order (indices into tasks)
+    std::vector<int32_t> pending;  // initial pending counter per vertex
+    int64_t total_tasks = 0;       // over all ranks
+};
+
+// schedule.cpp: tasks, broadcast flags, pending counters and claim order (needs VertexDesc
+// shape / tiling / part fields filled in).
+pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world, int rank, int nblocks,
+                           SchedPlan& out, std::string& err);
 constexpr int kTile = 8;     // max outputs per lane group along qstar
 constexpr int kCostRows = 64;  // edge-table rows per cost-table CTA
 
@@ -125,8 +150,9 @@ void launch_cost_tables(const pase_node* nodes_dev, const int32_t* K_dev, const 
 void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vertex,
                       const VertexDesc& vd_host, void* stream);
 void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, const TaskDesc* tasks_dev,
-                          const int32_t* order_dev, int ntasks, int32_t* sched_dev, int nblocks,
-                          int64_t* trace_dev, void* stream);
+                          const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
+                          const Peers& peers, int nblocks, int64_t* trace_dev, void* stream);
+void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev, void* stream);
 int persistent_blocks_per_sm();
 void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,
                       const double* root_T, int32_t* choice_dev, double* total_dev, void* stream);

@@ -1,0 +1,181 @@
+// schedule.cpp -- host-side task plan of the persistent DP kernel.
+//
+// Single GPU: each DP vertex's items are cut into tasks; the task DAG (a task of vertex p
+// waits for all tasks of p's children) is list-scheduled on the CTAs of the grid with
+// critical-path priority, giving a static claim order that is topological.
+//
+// Multi-GPU (world G > 1): a table with |T(i)| * 8 >= redundant_below bytes
+// and >= 2 coordinates is partitioned by contiguous ranges of its highest-rank coordinate
+// u_top(i) (configs [q*K/G, (q+1)*K/G) of u_top on rank q); smaller tables are computed
+// redundantly on every rank.  A partitioned child j whose parent p is partitioned on a
+// coordinate that is also in D(j) is partitioned identically (u_top(j) = u_top(p), since
+// D(j) ⊆ D(p) ∪ {sigma_p}), so p reads only local rows: no communication.  Otherwise the
+// child is "broadcast": its tasks write their outputs into every rank's copy of T(j)
+// (peer stores over NVLink, fused into the DP kernel) and decrement every rank's pending
+// counter of p.  Argmin tables of partitioned vertices are always broadcast, so every rank
+// can back-substitute locally.  One global list schedule over all ranks' tasks gives every
+// rank a claim order consistent with a single topological order: deadlock-free across
+// ranks (the globally earliest unfinished task always has its dependencies done and is
+// held or next to be claimed by its rank).
+#include <algorithm>
+#include <cstdio>
+#include <queue>
+
+#include "pase_internal.h"
+
+namespace pase {
+
+pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world, int rank, int nblocks,
+                           SchedPlan& out, std::string& err) {
+    const int n = P.n;
+    const int G = std::max(world, 1);
+    nblocks = std::max(nblocks, 1);
+    const int64_t spread = (int64_t)kTasksPerBlock * nblocks;
+    // ---- per (vertex, rank): unit runs, split into tasks
+    struct GTask { int32_t rank, vtx; int64_t i0, i1; };
+    std::vector<GTask> all;
+    std::vector<std::vector<std::vector<int32_t>>> tasks_of(n, std::vector<std::vector<int32_t>>(G));
+    for (int i = 0; i < n; ++i) {
+        const VertexDesc& d = vd[i];
+        const int64_t units = d.shape >= 0 ? d.nitems : d.nout;
+        const int64_t groups = 256 >> d.glog;
+        for (int q = 0; q < G; ++q) {
+            std::vector<std::pair<int64_t, int64_t>> runs;
+            if (!d.part) {
+                runs.push_back({0, units});
+            } else {
+                const int top = d.m - 1;
+                const int64_t Kt = d.radix[top];
+                const int64_t lo = q * Kt / G, hi = (q + 1) * Kt / G;
+                if (d.shape >= 0) {              // items = combo + ncombo * tile; top is combo's slowest
+                    const int64_t S = d.ncombo / Kt;
+                    for (int64_t xt = 0; xt < d.ntile; ++xt)
+                        if (hi > lo) runs.push_back({xt * d.ncombo + lo * S, xt * d.ncombo + hi * S});
+                } else {                         // items = outputs; top is the slowest coordinate
+                    const int64_t S = d.nout / Kt;
+                    if (hi > lo) runs.push_back({lo * S, hi * S});
+                }
+            }
+            int64_t local = 0;
+            for (auto& r : runs) local += r.second - r.first;
+            int64_t ti = std::max<int64_t>(groups, (local + spread - 1) / spread);
+            ti = (ti + groups - 1) / groups * groups;
+            for (auto& r : runs)
+                for (int64_t a = r.first; a < r.second; a += ti) {
+                    tasks_of[i][q].push_back((int32_t)all.size());
+                    all.push_back({q, i, a, std::min(r.second, a + ti)});
+                }
+        }
+    }
+    // ---- broadcast flags (bit 0: T, bit 1: A)
+    for (int j = 0; j < n; ++j) {
+        VertexDesc& d = vd[j];
+        d.bcast = 0;
+        if (!d.part) continue;
+        const int p = P.parent[j];
+        bool aligned = false;
+        if (p >= 0 && vd[p].part) {
+            const int top_p = P.dep[p][vd[p].m - 1];
+            aligned = std::find(P.dep[j].begin(), P.dep[j].end(), top_p) != P.dep[j].end();
+        }
+        d.bcast = (aligned ? 0 : 1) | 2;
+    }
+    // ---- pending counters per (rank, vertex): tasks each rank's copy of p waits for
+    auto waits_on = [&](int p, int q) -> int64_t {
+        int64_t s = 0;
+        for (int j : P.children[p]) {
+            if (vd[j].bcast & 1)
+                for (int r = 0; r < G; ++r) s += (int64_t)tasks_of[j][r].size();
+            else
+                s += (int64_t)tasks_of[j][q].size();
+        }
+        return s;
+    };
+    std::vector<std::vector<int64_t>> pend(G, std::vector<int64_t>(n));
+    for (int q = 0; q < G; ++q)
+        for (int p = 0; p < n; ++p) pend[q][p] = waits_on(p, q);
+    out.pending.assign(n, 0);
+    for (int p = 0; p < n; ++p) {
+        if (pend[rank][p] > INT32_MAX) { err = "internal: pending counter overflow"; return PASE_ERR_RESOURCE; }
+        out.pending[p] = (int32_t)pend[rank][p];
+    }
+    // ---- global list schedule: per-rank pools of nblocks CTAs, critical path first.
+    // Estimated task time: ~3 us dependent-latency overhead + candidates at ~3e9/s per CTA.
+    const int64_t ntk = (int64_t)all.size();
+    std::vector<double> tdur(ntk), bl(n, 0.0);
+    for (int64_t t = 0; t < ntk; ++t) {
+        const VertexDesc& d = vd[all[t].vtx];
+        const double cand = (double)(all[t].i1 - all[t].i0) * d.K * (d.shape >= 0 ? kTile : 1);
+        tdur[t] = 3.0 + cand / 3000.0;
+    }
+    for (int i = n - 1; i >= 0; --i) {                 // parents have higher ranks
+        double work = 0.0, longest = 0.0;
+        for (int q = 0; q < G; ++q)
+            for (int32_t t : tasks_of[i][q]) { work += tdur[t]; longest = std::max(longest, tdur[t]); }
+        const double vt = std::max(longest, work / ((double)nblocks * G));
+        bl[i] = vt + (P.parent[i] >= 0 ? bl[P.parent[i]] : 0.0);
+    }
+    std::vector<double> start(ntk, -1.0);
+    {
+        using RT = std::pair<double, int32_t>;                         // (priority, -task)
+        std::vector<std::priority_queue<RT>> ready(G);
+        using EV = std::pair<double, int32_t>;                         // (finish time, task)
+        std::priority_queue<EV, std::vector<EV>, std::greater<EV>> events;
+        auto release = [&](int v, int q) {
+            for (int32_t t : tasks_of[v][q]) ready[q].push({bl[v], -t});
+        };
+        for (int i = 0; i < n; ++i)
+            if (P.children[i].empty())
+                for (int q = 0; q < G; ++q) release(i, q);
+        std::vector<int> free_w(G, nblocks);
+        double now = 0.0;
+        int64_t started = 0;
+        while (started < ntk) {
+            for (int q = 0; q < G; ++q)
+                while (free_w[q] > 0 && !ready[q].empty()) {
+                    const int32_t t = -ready[q].top().second;
+                    ready[q].pop();
+                    start[t] = now;
+                    ++started;
+                    --free_w[q];
+                    events.push({now + tdur[t], t});
+                }
+            if (started == ntk) break;
+            if (events.empty()) { err = "internal: task DAG is not schedulable"; return PASE_ERR_STATE; }
+            const EV e = events.top();
+            events.pop();
+            now = e.first;
+            const GTask& gt = all[e.second];
+            ++free_w[gt.rank];
+            const int par = P.parent[gt.vtx];
+            if (par < 0) continue;
+            if (vd[gt.vtx].bcast & 1) {
+                for (int q = 0; q < G; ++q)
+                    if (--pend[q][par] == 0) release(par, q);
+            } else if (--pend[gt.rank][par] == 0) {
+                release(par, gt.rank);
+            }
+        }
+    }
+    // ---- this rank's tasks in simulated start order
+    std::vector<int32_t> mine;
+    for (int64_t t = 0; t < ntk; ++t)
+        if (all[t].rank == rank) mine.push_back((int32_t)t);
+    std::stable_sort(mine.begin(), mine.end(), [&](int32_t a, int32_t b) { return start[a] < start[b]; });
+    out.tasks.clear();
+    out.order.clear();
+    std::vector<int32_t> local_id(ntk, -1);       // local ids in vertex order
+    for (int i = 0; i < n; ++i) {
+        vd[i].task0 = (int32_t)out.tasks.size();
+        for (int32_t t : tasks_of[i][rank]) {
+            local_id[t] = (int32_t)out.tasks.size();
+            out.tasks.push_back({i, 0, all[t].i0, all[t].i1});
+        }
+        vd[i].ntasks = (int32_t)tasks_of[i][rank].size();
+    }
+    for (int32_t t : mine) out.order.push_back(local_id[t]);
+    out.total_tasks = ntk;
+    return PASE_OK;
+}
+
+}  // namespace pase

@@ -19,7 +19,7 @@ SO = os.path.join(HERE, "libpase.so")
 PASE_MAX_DIMS = 8
 PASE_MAX_HALO = 4
 PASE_MAX_DEP = 12
-PASE_UID_BYTES = 128
+PASE_HANDLE_BYTES = 256
 PASE_CFG_EXACT_P, PASE_CFG_LE_P = 0, 1
 STATUS = {0: "PASE_OK", 1: "PASE_ERR_INVALID", 2: "PASE_ERR_RESOURCE", 3: "PASE_ERR_CUDA",
           4: "PASE_ERR_NCCL", 5: "PASE_ERR_STATE"}
@@ -65,8 +65,8 @@ class pase_machine(C.Structure):
         ("cuda_device", C.c_int32),
         ("rank", C.c_int32),
         ("world", C.c_int32),
-        ("reserved1", C.c_int32),
-        ("nccl_unique_id", C.c_void_p),
+        ("virtual_ranks", C.c_int32),
+        ("reserved", C.c_void_p),
         ("cuda_stream", C.c_void_p),
     ]
 
@@ -87,8 +87,8 @@ class pase_stats(C.Structure):
 
 EXPORTS = ["pase_create", "pase_solve", "pase_get_stats", "pase_last_error", "pase_destroy",
            "pase_get_configs", "pase_get_order", "pase_get_cost_tables", "pase_get_dp_table",
-           "pase_table_entries", "pase_set_cost_tables", "pase_set_profiling", "pase_get_unique_id",
-           "pase_get_trace"]
+           "pase_table_entries", "pase_set_cost_tables", "pase_set_profiling", "pase_get_trace",
+           "pase_launch", "pase_finish", "pase_export_handle", "pase_connect", "pase_get_schedule"]
 
 _lib = None
 
@@ -124,12 +124,17 @@ def load(path: str = SO):
     L.pase_table_entries.restype = C.c_int64
     L.pase_set_cost_tables.argtypes = [ctx_p, P(C.c_double), P(C.c_double)]
     L.pase_set_profiling.argtypes = [ctx_p, C.c_int32]
-    L.pase_get_unique_id.argtypes = [C.c_void_p]
     L.pase_get_trace.argtypes = [ctx_p, P(C.c_int64), C.c_int64]
     L.pase_get_trace.restype = C.c_int64
+    L.pase_launch.argtypes = [ctx_p]
+    L.pase_finish.argtypes = [ctx_p, P(C.c_int32), P(C.c_int32), P(C.c_double)]
+    L.pase_export_handle.argtypes = [ctx_p, C.c_void_p]
+    L.pase_connect.argtypes = [ctx_p, C.c_void_p]
+    L.pase_get_schedule.argtypes = [ctx_p, P(C.c_int32), P(C.c_int64), P(C.c_int32)]
+    L.pase_get_schedule.restype = C.c_int64
     for f in ("pase_create", "pase_solve", "pase_get_stats", "pase_get_configs", "pase_get_order",
               "pase_get_cost_tables", "pase_get_dp_table", "pase_set_cost_tables", "pase_set_profiling",
-              "pase_get_unique_id"):
+              "pase_launch", "pase_finish", "pase_export_handle", "pase_connect"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -185,7 +190,7 @@ def marshal_graph(graph: dict):
 
 def make_machine(flops: float = 1e13, bandwidth: float = 1e10, policy: int = PASE_CFG_EXACT_P,
                  device: int = 0, stream: Optional[int] = None, rank: int = 0, world: int = 1,
-                 uid: Optional[bytes] = None, table_budget: int = 0,
+                 virtual_ranks: bool = False, table_budget: int = 0,
                  redundant_below: int = 4 << 20, ordering: int = 0) -> pase_machine:
     m = pase_machine()
     m.flops_per_device, m.link_bandwidth = float(flops), float(bandwidth)
@@ -194,8 +199,7 @@ def make_machine(flops: float = 1e13, bandwidth: float = 1e10, policy: int = PAS
     m.table_budget_bytes = int(table_budget)
     m.redundant_below_bytes = int(redundant_below)
     m.cuda_device, m.rank, m.world = int(device), int(rank), int(world)
-    m._uid = C.create_string_buffer(uid, PASE_UID_BYTES) if uid else None
-    m.nccl_unique_id = C.cast(m._uid, C.c_void_p) if uid else None
+    m.virtual_ranks = 1 if virtual_ranks else 0
     m.cuda_stream = stream
     return m
 
@@ -205,7 +209,7 @@ class Context:
 
     def __init__(self, graph: dict, p: int, policy="exact_p", flops: Optional[float] = None,
                  bandwidth: Optional[float] = None, device: int = 0, stream: Optional[int] = None,
-                 rank: int = 0, world: int = 1, uid: Optional[bytes] = None, table_budget: int = 0,
+                 rank: int = 0, world: int = 1, virtual_ranks: bool = False, table_budget: int = 0,
                  redundant_below: int = 4 << 20, ordering="sortnodes"):
         L = load()
         mach_d = graph.get("machine") or {}
@@ -216,8 +220,9 @@ class Context:
         self.n, self.m = len(graph["nodes"]), len(graph["edges"])
         g, self._keep = marshal_graph(graph)
         order = ORDERINGS[ordering] if isinstance(ordering, str) else int(ordering)
-        self._mach = make_machine(flops, bandwidth, pol, device, stream, rank, world, uid, table_budget,
-                                  redundant_below, order)
+        self._mach = make_machine(flops, bandwidth, pol, device, stream, rank, world, virtual_ranks,
+                                  table_budget, redundant_below, order)
+        self.rank, self.world = rank, world
         h = C.c_void_p()
         st = L.pase_create(C.byref(g), int(p), C.byref(self._mach), C.byref(h))
         if st != 0:
@@ -254,6 +259,39 @@ class Context:
         self._chk(self._L.pase_solve(self._h, _ptr(cfg, C.c_int32), _ptr(idx, C.c_int32), C.byref(tot)))
         tuples = [tuple(int(c) for c in cfg[v, :len(self.graph["nodes"][v]["dims"])]) for v in range(self.n)]
         return {"cost": tot.value, "config_index": idx, "configs": tuples}
+
+    def launch(self) -> None:
+        """pase_launch: enqueue one solve (a multi-GPU group launches every rank first)."""
+        self._chk(self._L.pase_launch(self._h))
+
+    def finish(self) -> Dict[str, object]:
+        """pase_finish: wait for the launched solve; same result as solve()."""
+        cfg = np.zeros((self.n, PASE_MAX_DIMS), np.int32)
+        idx = np.zeros(self.n, np.int32)
+        tot = C.c_double()
+        self._chk(self._L.pase_finish(self._h, _ptr(cfg, C.c_int32), _ptr(idx, C.c_int32), C.byref(tot)))
+        tuples = [tuple(int(c) for c in cfg[v, :len(self.graph["nodes"][v]["dims"])]) for v in range(self.n)]
+        return {"cost": tot.value, "config_index": idx, "configs": tuples}
+
+    def export_handle(self) -> bytes:
+        buf = C.create_string_buffer(PASE_HANDLE_BYTES)
+        self._chk(self._L.pase_export_handle(self._h, buf))
+        return buf.raw
+
+    def connect(self, handles: Sequence[bytes]) -> None:
+        """pase_connect with the group's handles ordered by rank."""
+        blob = b"".join(handles)
+        buf = C.create_string_buffer(blob, len(blob))
+        self._chk(self._L.pase_connect(self._h, buf))
+
+    def schedule(self) -> Dict[str, np.ndarray]:
+        """pase_get_schedule: per-vertex (part, bcast, ntasks, pending), tasks, claim order."""
+        nt = self._L.pase_get_schedule(self._h, None, None, None)
+        vinfo = np.zeros((self.n, 4), np.int32)
+        tasks = np.zeros((max(nt, 1), 3), np.int64)
+        order = np.zeros(max(nt, 1), np.int32)
+        self._L.pase_get_schedule(self._h, _ptr(vinfo, C.c_int32), _ptr(tasks, C.c_int64), _ptr(order, C.c_int32))
+        return {"vinfo": vinfo, "tasks": tasks[:nt], "order": order[:nt]}
 
     def stats(self) -> Dict[str, float]:
         s = pase_stats()
@@ -330,13 +368,27 @@ class Context:
         self._chk(self._L.pase_set_cost_tables(self._h, _ptr(L, C.c_double), _ptr(W, C.c_double)))
 
 
-def unique_id() -> bytes:
-    """pase_get_unique_id: NCCL unique id bytes for multi-GPU contexts (rank 0)."""
-    buf = C.create_string_buffer(PASE_UID_BYTES)
-    st = load().pase_get_unique_id(buf)
-    if st != 0:
-        raise PaseError(st, "pase_get_unique_id failed")
-    return buf.raw
+def virtual_group(graph: dict, p: int, world: int, device: int = 0, **kw) -> List[Context]:
+    """A multi-GPU group of `world` ranks sharing one device in this process (testing the
+    partitioned path on a single GPU): create, export, connect."""
+    import torch
+    ctxs = []
+    for r in range(world):
+        st = torch.cuda.Stream(device=device)
+        ctxs.append(Context(graph, p, device=device, rank=r, world=world, virtual_ranks=True,
+                            stream=st.cuda_stream, **kw))
+        ctxs[-1]._torch_stream = st
+    handles = [c.export_handle() for c in ctxs]
+    for c in ctxs:
+        c.connect(handles)
+    return ctxs
+
+
+def solve_group(ctxs: Sequence[Context]) -> List[Dict[str, object]]:
+    """Launch every rank of a (virtual) group, then wait for all."""
+    for c in ctxs:
+        c.launch()
+    return [c.finish() for c in ctxs]
 
 
 # C-ABI-named wrappers (same names as include/pase.h)

@@ -52,7 +52,7 @@ int main(void) {
   printf("%zu %zu %zu %zu %zu\\n", sizeof(pase_node), sizeof(pase_edge), sizeof(pase_graph),
          sizeof(pase_machine), sizeof(pase_stats));
   printf("%zu %zu %zu %zu\\n", offsetof(pase_node, flops_per_point), offsetof(pase_node, elem_bytes),
-         offsetof(pase_machine, nccl_unique_id), offsetof(pase_stats, ms_create));
+         offsetof(pase_machine, reserved), offsetof(pase_stats, ms_create));
   return 0;
 }
 """)
@@ -64,7 +64,7 @@ int main(void) {
                      C.sizeof(pase.pase_machine), C.sizeof(pase.pase_stats)]
     offs = [int(x) for x in lines[1].split()]
     assert offs == [pase.pase_node.flops_per_point.offset, pase.pase_node.elem_bytes.offset,
-                    pase.pase_machine.nccl_unique_id.offset, pase.pase_stats.ms_create.offset]
+                    pase.pase_machine.reserved.offset, pase.pase_stats.ms_create.offset]
 
 
 def check_plan_against_oracle(graph, p, policy):

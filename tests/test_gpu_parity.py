@@ -201,3 +201,38 @@ def test_bfs_ordering_gpu():
         K = np.array([len(c) for c in O.configs(g, p, O.LE_P)], np.int32)
         Ls, Ws = random_costs(g, K, seed, "real")
         run_pair(g, p, "le_p", Ls, Ws, ordering="bfs")
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_virtual_multi_gpu_group(world):
+    """SURVEY §8.e on one GPU: `world` ranks share the device (virtual_ranks).  Big tables are
+    partitioned by their top coordinate, broadcast partitions are written into the peers'
+    tables by the DP kernel itself, every rank back-substitutes locally.  Every rank must
+    return the oracle's strategy and cost bit for bit; argmin tables are complete on every
+    rank; T tables complete wherever they are replicated or broadcast, and on the owned
+    partition otherwise."""
+    for name, thr in (("transformer", 1 << 16), ("inception_v3", 1 << 12), ("gnmt", 1 << 16)):
+        g, p = zoo.bench_graph(name)
+        ctxs = pase.virtual_group(g, p, world, redundant_below=thr)
+        P = O.Problem.from_model(g, p)
+        o = P.dp(threads=THREADS, want_tables=True)
+        for rep in range(2):                                   # group barriers across solves
+            res = pase.solve_group(ctxs)
+            for r in res:
+                assert list(r["config_index"]) == list(o["strategy"]), name
+                assert np.float64(r["cost"]).view(np.uint64) == np.float64(o["cost"]).view(np.uint64)
+        off = o["toff"]
+        nparts = 0
+        for c in ctxs:
+            sch = c.schedule()
+            nparts += int(sch["vinfo"][:, 0].sum())
+            for i in range(P.n):
+                T, A = c.dp_table(i)
+                oT, oA = o["T"][off[i]:off[i + 1]], o["A"][off[i]:off[i + 1]]
+                assert np.array_equal(A.astype(np.int32), oA), (name, c.rank, i)
+                part, bcast = int(sch["vinfo"][i, 0]), int(sch["vinfo"][i, 1])
+                if not part or (bcast & 1):
+                    assert np.array_equal(T.view(np.uint64), oT.view(np.uint64)), (name, c.rank, i)
+        assert nparts > 0
+        for c in ctxs:
+            c.close()
