@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -30,6 +31,8 @@ struct pase_ctx {
     bool virtual_ranks = false;             // all ranks of the group share this device
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    bool async_pools = false;               // pools from the library's stream-ordered mempool
+    bool big_pinned = false;                // h_total came from cudaMallocHost, not the cache
     std::vector<cudaStream_t> aux;          // fork streams (per-vertex launch schedule)
     // pool 1: inputs, cost tables, DP tables (T/A written by peers), descriptors
     void* pool = nullptr;
@@ -81,6 +84,7 @@ struct pase_ctx {
     bool solved = false;
     bool launched = false;
     bool no_graph = false;
+    int direct_left = 1;                    // solves to issue directly before capturing
     int profiling = 0;
     cudaGraphExec_t exec = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr, ev_dp = nullptr;
@@ -102,6 +106,57 @@ thread_local std::string g_create_err;
     } while (0)
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Device memory of single-process contexts comes from one stream-ordered pool per device
+// that keeps freed memory cached (release threshold = max): a create/solve/destroy cycle
+// then costs no cudaMalloc/cudaFree (each of which maps/unmaps pages and synchronises).
+// Contexts of a multi-process group use cudaMalloc (their pools are exported over CUDA IPC).
+std::mutex g_pool_mu;
+cudaMemPool_t g_mempool[64] = {};
+
+cudaMemPool_t device_mempool(int dev) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!g_mempool[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t mp = nullptr;
+        if (cudaMemPoolCreate(&mp, &props) != cudaSuccess) return nullptr;
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
+        g_mempool[dev] = mp;
+    }
+    return g_mempool[dev];
+}
+
+// Pinned result blocks (total | err | choice[n]) are recycled through a small process-wide
+// cache: cudaMallocHost/cudaFreeHost cost milliseconds (and cudaFreeHost synchronises).
+constexpr size_t kPinnedBlock = 64 << 10;
+std::vector<void*> g_pinned_free;
+
+void* pinned_get(size_t bytes, bool* big) {
+    *big = bytes > kPinnedBlock;
+    if (!*big) {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (!g_pinned_free.empty()) {
+            void* p = g_pinned_free.back();
+            g_pinned_free.pop_back();
+            return p;
+        }
+    }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, *big ? bytes : kPinnedBlock) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void pinned_put(void* p, bool big) {
+    if (!p) return;
+    if (big) { cudaFreeHost(p); return; }
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pinned_free.push_back(p);
+}
 
 // Cost-table work list: edges first (row chunks of the later-endpoint configs), then vertices.
 std::vector<pase::CostChunk> cost_chunks(const Plan& P) {
@@ -138,7 +193,13 @@ pase_status carve(pase_ctx* ctx, std::vector<Item>& items, void** base, size_t* 
     for (auto& it : items) total += align_up(it.bytes);
     total = std::max<size_t>(total, 256);
     if (device) {
-        cudaError_t e = cudaMalloc(base, total);
+        cudaError_t e = cudaErrorMemoryAllocation;
+        if (ctx->async_pools) {
+            cudaMemPool_t mp = device_mempool(ctx->dev);
+            e = mp ? cudaMallocFromPoolAsync(base, total, mp, ctx->stream) : cudaErrorMemoryAllocation;
+        } else {
+            e = cudaMalloc(base, total);
+        }
         if (e != cudaSuccess) {
             ctx->err = std::string("cudaMalloc of ") + std::to_string(total) + " bytes failed: " + cudaGetErrorString(e);
             return PASE_ERR_RESOURCE;
@@ -160,6 +221,7 @@ pase_status allocate(pase_ctx* ctx, bool device) {
     for (int i = 0; i < n; ++i) nterms_total += 1 + (int64_t)P.egt[i].size() + (int64_t)P.children[i].size();
     const int64_t ncfg = P.cfg_off[n];
     ctx->nchunks = (int)cost_chunks(P).size();
+    // uploaded items first: prepare() stages them in one host image and copies it once
     std::vector<Item> items = {
         {(void**)&ctx->d_nodes, sizeof(pase_node) * n},
         {(void**)&ctx->d_K, sizeof(int32_t) * n},
@@ -168,14 +230,14 @@ pase_status allocate(pase_ctx* ctx, bool device) {
         {(void**)&ctx->d_loff, sizeof(int64_t) * (n + 1)},
         {(void**)&ctx->d_edges, sizeof(EdgeDesc) * std::max(m, 1)},
         {(void**)&ctx->d_chunks, sizeof(pase::CostChunk) * (size_t)ctx->nchunks},
-        {(void**)&ctx->d_L, sizeof(double) * P.loff[n]},
-        {(void**)&ctx->d_W, sizeof(double) * std::max<int64_t>(P.woff[m], 1)},
-        {(void**)&ctx->d_T, sizeof(double) * P.toff[n]},
-        {(void**)&ctx->d_A, sizeof(uint16_t) * P.toff[n]},
         {(void**)&ctx->d_vd, sizeof(VertexDesc) * n},
         {(void**)&ctx->d_td, sizeof(TermDesc) * nterms_total},
         {(void**)&ctx->d_bt, sizeof(pase::BtDesc) * n},
         {(void**)&ctx->d_bt_off, sizeof(int32_t) * (n + 1)},
+        {(void**)&ctx->d_L, sizeof(double) * P.loff[n]},
+        {(void**)&ctx->d_W, sizeof(double) * std::max<int64_t>(P.woff[m], 1)},
+        {(void**)&ctx->d_T, sizeof(double) * P.toff[n]},
+        {(void**)&ctx->d_A, sizeof(uint16_t) * P.toff[n]},
         {(void**)&ctx->d_choice, sizeof(int32_t) * n},
         {(void**)&ctx->d_total, sizeof(double)},
     };
@@ -303,12 +365,12 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     // pool 2
     const size_t sched_words = pase::kSchedLine + (size_t)n;
     ctx->sched_bytes = sizeof(int32_t) * sched_words;
-    std::vector<Item> items2 = {
-        {(void**)&ctx->d_sched, ctx->sched_bytes},
+    std::vector<Item> items2 = {                          // uploaded items first, as pool 1
         {(void**)&ctx->d_sched_init, ctx->sched_bytes},
-        {(void**)&ctx->d_bar, sizeof(int32_t) * 3 * pase::kSchedLine},
         {(void**)&ctx->d_tasks, sizeof(pase::TaskDesc) * std::max<size_t>(ctx->sp.tasks.size(), 1)},
         {(void**)&ctx->d_order, sizeof(int32_t) * std::max<size_t>(ctx->sp.order.size(), 1)},
+        {(void**)&ctx->d_sched, ctx->sched_bytes},
+        {(void**)&ctx->d_bar, sizeof(int32_t) * 3 * pase::kSchedLine},
         {(void**)&ctx->d_trace, trace_on() ? sizeof(int64_t) * 4 * std::max<size_t>(ctx->sp.tasks.size(), 1) : 0},
     };
     if ((st = carve(ctx, items2, &ctx->pool2, &ctx->pool2_bytes, device))) return st;
@@ -345,30 +407,35 @@ pase_status prepare(pase_ctx* ctx, bool device) {
         }
     }
     ctx->nbtlev = nlev;
-    ctx->h2d_bytes = sizeof(pase_node) * n + sizeof(int32_t) * n + sizeof(int64_t) * (n + 1) * 2 +
-                     sizeof(int32_t) * P.cfg.size() + sizeof(EdgeDesc) * ed.size() +
-                     sizeof(pase::CostChunk) * chunks.size() + sizeof(VertexDesc) * n +
-                     sizeof(TermDesc) * ctx->td.size() + sizeof(pase::BtDesc) * n + sizeof(int32_t) * (nlev + 1) +
-                     sizeof(pase::TaskDesc) * ctx->sp.tasks.size() + ctx->sched_bytes +
-                     sizeof(int32_t) * ctx->sp.order.size();
+    // one host image per pool (the uploaded prefix), one copy each
+    auto stage = [](std::vector<char>& img, void* pool, void* dst, const void* src, size_t bytes) {
+        const size_t off = (size_t)((char*)dst - (char*)pool);
+        if (off + bytes > img.size()) img.resize(off + bytes);
+        if (bytes) std::memcpy(img.data() + off, src, bytes);
+    };
+    std::vector<char> img1, img2;
+    img1.reserve((size_t)((char*)ctx->d_L - (char*)ctx->pool));
+    img2.reserve((size_t)((char*)ctx->d_sched - (char*)ctx->pool2));
+    stage(img1, ctx->pool, ctx->d_nodes, P.nodes.data(), sizeof(pase_node) * n);
+    stage(img1, ctx->pool, ctx->d_K, P.K.data(), sizeof(int32_t) * n);
+    stage(img1, ctx->pool, ctx->d_cfg_off, P.cfg_off.data(), sizeof(int64_t) * (n + 1));
+    stage(img1, ctx->pool, ctx->d_cfg, P.cfg.data(), sizeof(int32_t) * P.cfg.size());
+    stage(img1, ctx->pool, ctx->d_loff, P.loff.data(), sizeof(int64_t) * (n + 1));
+    stage(img1, ctx->pool, ctx->d_edges, ed.data(), sizeof(EdgeDesc) * ed.size());
+    stage(img1, ctx->pool, ctx->d_chunks, chunks.data(), sizeof(pase::CostChunk) * chunks.size());
+    stage(img1, ctx->pool, ctx->d_vd, ctx->vd.data(), sizeof(VertexDesc) * n);
+    stage(img1, ctx->pool, ctx->d_td, ctx->td.data(), sizeof(TermDesc) * ctx->td.size());
+    stage(img1, ctx->pool, ctx->d_bt, bt.data(), sizeof(pase::BtDesc) * n);
+    stage(img1, ctx->pool, ctx->d_bt_off, bt_off.data(), sizeof(int32_t) * (nlev + 1));
+    stage(img2, ctx->pool2, ctx->d_sched_init, sched.data(), ctx->sched_bytes);
+    stage(img2, ctx->pool2, ctx->d_tasks, ctx->sp.tasks.data(), sizeof(pase::TaskDesc) * ctx->sp.tasks.size());
+    stage(img2, ctx->pool2, ctx->d_order, ctx->sp.order.data(), sizeof(int32_t) * ctx->sp.order.size());
+    ctx->h2d_bytes = img1.size() + img2.size();
     if (!device) return PASE_OK;
-    cudaStream_t s = ctx->stream;
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_nodes, P.nodes.data(), sizeof(pase_node) * n, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_K, P.K.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_cfg_off, P.cfg_off.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_cfg, P.cfg.data(), sizeof(int32_t) * P.cfg.size(), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_loff, P.loff.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_edges, ed.data(), sizeof(EdgeDesc) * ed.size(), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_chunks, chunks.data(), sizeof(pase::CostChunk) * chunks.size(), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_vd, ctx->vd.data(), sizeof(VertexDesc) * n, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_td, ctx->td.data(), sizeof(TermDesc) * ctx->td.size(), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_tasks, ctx->sp.tasks.data(), sizeof(pase::TaskDesc) * ctx->sp.tasks.size(), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_order, ctx->sp.order.data(), sizeof(int32_t) * ctx->sp.order.size(), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_sched_init, sched.data(), ctx->sched_bytes, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemsetAsync(ctx->d_bar, 0, sizeof(int32_t) * 3 * pase::kSchedLine, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_bt, bt.data(), sizeof(pase::BtDesc) * n, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_bt_off, bt_off.data(), sizeof(int32_t) * (nlev + 1), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaStreamSynchronize(s));   // host vectors above are stack-local
+    // pageable sources: the calls return once the images are staged, so they may go out of scope
+    CUDA_TRY(cudaMemcpyAsync(ctx->pool, img1.data(), img1.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx->pool2, img2.data(), img2.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(ctx->d_bar, 0, sizeof(int32_t) * 3 * pase::kSchedLine, ctx->stream));
     return PASE_OK;
 }
 
@@ -379,15 +446,15 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
     const Plan& P = ctx->P;
     const int n = P.n;
     if (capture && ctx->exec) { cudaGraphExecDestroy(ctx->exec); ctx->exec = nullptr; }
-    const int nstreams = 4;
-    if (ctx->aux.empty()) {
+    const int nstreams = ctx->persistent ? 0 : 4;
+    if (ctx->aux.empty() && nstreams) {
         ctx->aux.resize(nstreams);
         for (auto& s : ctx->aux) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     }
     std::vector<cudaEvent_t> done(ctx->persistent ? 0 : n);
     for (auto& e : done) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    cudaEvent_t start;
-    CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    cudaEvent_t start = nullptr;
+    if (!ctx->persistent) CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
     std::vector<cudaEvent_t> join(nstreams);
     for (auto& e : join) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     cudaStream_t s = ctx->stream;
@@ -437,7 +504,7 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
     if (capture) ce = cudaStreamEndCapture(s, &graph);
     for (auto& e : done) cudaEventDestroy(e);
     for (auto& e : join) cudaEventDestroy(e);
-    cudaEventDestroy(start);
+    if (start) cudaEventDestroy(start);
     if (ce != cudaSuccess) { ctx->err = std::string("stream capture: ") + cudaGetErrorString(ce); return PASE_ERR_CUDA; }
     if (capture) {
         ce = cudaGraphInstantiate(&ctx->exec, graph, 0);
@@ -447,15 +514,18 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
     return PASE_OK;
 }
 
-// The solve schedule is recorded once as a CUDA graph (multi-GPU: after pase_connect);
-// PASE_NO_GRAPH=1 issues it directly at every solve instead (kernels then launch in order).
+// The solve schedule is issued directly at the first solve after a (re)configuration and
+// recorded as a CUDA graph at the second (a context solved once -- the create/solve/destroy
+// pattern -- never pays for capture and instantiation); PASE_NO_GRAPH=1 issues it directly
+// at every solve.
 pase_status record_graph(pase_ctx* ctx) {
     const int dp_launches = ctx->persistent ? 1 + (ctx->world > 1 ? 2 : 0) : ctx->P.n;
     ctx->stats.n_launches = (ctx->override_tables ? 0 : 1) + dp_launches + 1;
     const char* ng = std::getenv("PASE_NO_GRAPH");
     ctx->no_graph = ng && ng[0] == '1';
-    if (ctx->no_graph || (ctx->world > 1 && !ctx->connected)) return PASE_OK;
-    return issue_schedule(ctx, true);
+    if (ctx->exec) { cudaGraphExecDestroy(ctx->exec); ctx->exec = nullptr; }
+    ctx->direct_left = 1;
+    return PASE_OK;
 }
 
 void fill_stats(pase_ctx* ctx) {
@@ -542,8 +612,13 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
     }
     if (!device) {                          // host-only planning context (no device work)
         ctx->nblocks = std::max(1, 2 * 148 / (ctx->virtual_ranks ? ctx->world : 1));
+        auto ta = std::chrono::steady_clock::now();
         if ((st = allocate(ctx, false))) return fail(st);
         if ((st = prepare(ctx, false))) return fail(st);
+        if (const char* tv = std::getenv("PASE_TIMING"); tv && tv[0] == '1')
+            std::fprintf(stderr, "[pase] host-only create: plan %.3f ms, prepare %.3f ms\n",
+                         std::chrono::duration<double, std::milli>(ta - t0).count(),
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta).count());
         fill_stats(ctx);
         ctx->stats.n_launches = 0;
         ctx->stats.ms_create =
@@ -564,11 +639,15 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
         }
         ctx->own_stream = true;
     }
-    if (cudaMallocHost(&ctx->h_choice, sizeof(int32_t) * ctx->P.n) != cudaSuccess ||
-        cudaMallocHost(&ctx->h_total, sizeof(double)) != cudaSuccess ||
-        cudaMallocHost(&ctx->h_err, sizeof(int32_t)) != cudaSuccess) {
-        ctx->err = "cudaMallocHost failed";
-        return fail(PASE_ERR_CUDA);
+    {                                       // one pinned block: total | err | choice[n]
+        void* h = pinned_get(16 + sizeof(int32_t) * ctx->P.n, &ctx->big_pinned);
+        if (!h) {
+            ctx->err = "cudaMallocHost failed";
+            return fail(PASE_ERR_CUDA);
+        }
+        ctx->h_total = (double*)h;
+        ctx->h_err = (int32_t*)((char*)h + 8);
+        ctx->h_choice = (int32_t*)((char*)h + 16);
     }
     if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
         cudaEventCreate(&ctx->ev_mid) != cudaSuccess || cudaEventCreate(&ctx->ev_dp) != cudaSuccess) {
@@ -586,12 +665,16 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
         ctx->nblocks = std::max(1, std::max(1, pase::persistent_blocks_per_sm()) * sms /
                                        (ctx->virtual_ranks ? ctx->world : 1));
     }
+    ctx->async_pools = ctx->world == 1;     // groups export their pools (CUDA IPC / peer access)
     auto t_plan = std::chrono::steady_clock::now();
     if ((st = allocate(ctx, true))) return fail(st);
     auto t_alloc = std::chrono::steady_clock::now();
     if ((st = prepare(ctx, true))) return fail(st);
     auto t_upload = std::chrono::steady_clock::now();
     if ((st = record_graph(ctx))) return fail(st);
+    // the pools are complete before any other stream (a peer's, the legacy one used by the
+    // introspection hooks) touches them
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) { ctx->err = "cudaStreamSynchronize failed"; return fail(PASE_ERR_CUDA); }
     auto t_graph = std::chrono::steady_clock::now();
     fill_stats(ctx);
     using ms = std::chrono::duration<double, std::milli>;
@@ -608,13 +691,18 @@ pase_status pase_launch(pase_ctx* ctx) {
     if (!ctx) return PASE_ERR_INVALID;
     if (ctx->dev < 0) { ctx->err = "host-only planning context: no solve"; return PASE_ERR_STATE; }
     if (ctx->world > 1 && !ctx->connected) { ctx->err = "multi-GPU context: call pase_connect first"; return PASE_ERR_STATE; }
-    if (!ctx->exec && !ctx->no_graph) { ctx->err = "context has no solve schedule"; return PASE_ERR_STATE; }
     if (ctx->launched) { ctx->err = "pase_launch called twice without pase_finish"; return PASE_ERR_STATE; }
     CUDA_TRY(cudaSetDevice(ctx->dev));
+    const bool direct = ctx->no_graph || ctx->direct_left > 0;
+    if (!direct && !ctx->exec) {
+        pase_status st = issue_schedule(ctx, true);
+        if (st) return st;
+    }
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
-    if (ctx->no_graph) {
+    if (direct) {
         pase_status st = issue_schedule(ctx, false);
         if (st) return st;
+        if (ctx->direct_left > 0) --ctx->direct_left;
     } else {
         CUDA_TRY(cudaGraphLaunch(ctx->exec, ctx->stream));
     }
@@ -675,8 +763,10 @@ pase_status pase_export_handle(const pase_ctx* ctx_c, void* blob) {
     h.n = ctx->P.n;
     h.total_tasks = ctx->total_tasks;
     CUDA_TRY(cudaSetDevice(ctx->dev));
-    CUDA_TRY(cudaIpcGetMemHandle(&h.h1, ctx->pool));
-    CUDA_TRY(cudaIpcGetMemHandle(&h.h2, ctx->pool2));
+    if (!ctx->async_pools) {
+        CUDA_TRY(cudaIpcGetMemHandle(&h.h1, ctx->pool));
+        CUDA_TRY(cudaIpcGetMemHandle(&h.h2, ctx->pool2));
+    }
     h.raw1 = (uint64_t)(uintptr_t)ctx->pool;
     h.raw2 = (uint64_t)(uintptr_t)ctx->pool2;
     h.off_T = (uint64_t)((char*)ctx->d_T - (char*)ctx->pool);
@@ -789,11 +879,14 @@ void pase_destroy(pase_ctx* ctx) {
     if (ctx->ev_mid) cudaEventDestroy(ctx->ev_mid);
     if (ctx->ev_dp) cudaEventDestroy(ctx->ev_dp);
     for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
-    if (ctx->pool) cudaFree(ctx->pool);
-    if (ctx->pool2) cudaFree(ctx->pool2);
-    if (ctx->h_choice) cudaFreeHost(ctx->h_choice);
-    if (ctx->h_total) cudaFreeHost(ctx->h_total);
-    if (ctx->h_err) cudaFreeHost(ctx->h_err);
+    if (ctx->async_pools) {                 // back to the cached pool, ordered after our work
+        if (ctx->pool) cudaFreeAsync(ctx->pool, ctx->stream);
+        if (ctx->pool2) cudaFreeAsync(ctx->pool2, ctx->stream);
+    } else {
+        if (ctx->pool) cudaFree(ctx->pool);
+        if (ctx->pool2) cudaFree(ctx->pool2);
+    }
+    pinned_put(ctx->h_total, ctx->big_pinned);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

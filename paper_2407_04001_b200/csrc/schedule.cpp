@@ -18,7 +18,9 @@
 // ranks (the globally earliest unfinished task always has its dependencies done and is
 // held or next to be claimed by its rank).
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <queue>
 
 #include "pase_internal.h"
@@ -31,6 +33,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     const int G = std::max(world, 1);
     nblocks = std::max(nblocks, 1);
     const int64_t spread = (int64_t)kTasksPerBlock * nblocks;
+    const auto tt0 = std::chrono::steady_clock::now();
     // ---- per (vertex, rank): unit runs, split into tasks
     struct GTask { int32_t rank, vtx; int64_t i0, i1; };
     std::vector<GTask> all;
@@ -115,14 +118,19 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         const double vt = std::max(longest, work / ((double)nblocks * G));
         bl[i] = vt + (P.parent[i] >= 0 ? bl[P.parent[i]] : 0.0);
     }
+    const auto tt1 = std::chrono::steady_clock::now();
     std::vector<double> start(ntk, -1.0);
     {
-        using RT = std::pair<double, int32_t>;                         // (priority, -task)
+        // ready (vertex, rank) runs: all tasks of a vertex share its priority, so the heap holds
+        // one entry per released run and a cursor walks the run's tasks
+        using RT = std::pair<double, int32_t>;                         // (priority, -(v*G+q))
         std::vector<std::priority_queue<RT>> ready(G);
-        using EV = std::pair<double, int32_t>;                         // (finish time, task)
+        std::vector<int32_t> cursor((size_t)n * G, 0);
+        // an event finishes k equal-length tasks of one run started at the same time
+        struct EV { double t; int32_t vq, k; bool operator>(const EV& o) const { return t != o.t ? t > o.t : vq > o.vq; } };
         std::priority_queue<EV, std::vector<EV>, std::greater<EV>> events;
         auto release = [&](int v, int q) {
-            for (int32_t t : tasks_of[v][q]) ready[q].push({bl[v], -t});
+            if (!tasks_of[v][q].empty()) ready[q].push({bl[v], -(v * G + q)});
         };
         for (int i = 0; i < n; ++i)
             if (P.children[i].empty())
@@ -133,30 +141,41 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         while (started < ntk) {
             for (int q = 0; q < G; ++q)
                 while (free_w[q] > 0 && !ready[q].empty()) {
-                    const int32_t t = -ready[q].top().second;
-                    ready[q].pop();
-                    start[t] = now;
-                    ++started;
-                    --free_w[q];
-                    events.push({now + tdur[t], t});
+                    const int32_t vq = -ready[q].top().second;
+                    const auto& run = tasks_of[vq / G][q];
+                    const double d = tdur[run[cursor[vq]]];
+                    int32_t k = 0;
+                    while (k < free_w[q] && cursor[vq] < (int32_t)run.size() && tdur[run[cursor[vq]]] == d) {
+                        start[run[cursor[vq]++]] = now;
+                        ++k;
+                    }
+                    if (cursor[vq] == (int32_t)run.size()) ready[q].pop();
+                    started += k;
+                    free_w[q] -= k;
+                    events.push({now + d, vq, k});
                 }
             if (started == ntk) break;
             if (events.empty()) { err = "internal: task DAG is not schedulable"; return PASE_ERR_STATE; }
             const EV e = events.top();
             events.pop();
-            now = e.first;
-            const GTask& gt = all[e.second];
-            ++free_w[gt.rank];
-            const int par = P.parent[gt.vtx];
+            now = e.t;
+            const int v = e.vq / G, q0 = e.vq % G;
+            free_w[q0] += e.k;
+            const int par = P.parent[v];
             if (par < 0) continue;
-            if (vd[gt.vtx].bcast & 1) {
+            if (vd[v].bcast & 1) {
                 for (int q = 0; q < G; ++q)
-                    if (--pend[q][par] == 0) release(par, q);
-            } else if (--pend[gt.rank][par] == 0) {
-                release(par, gt.rank);
+                    if ((pend[q][par] -= e.k) == 0) release(par, q);
+            } else if ((pend[q0][par] -= e.k) == 0) {
+                release(par, q0);
             }
         }
     }
+    const auto tt2 = std::chrono::steady_clock::now();
+    if (const char* tv = std::getenv("PASE_TIMING"); tv && tv[0] == '1')
+        std::fprintf(stderr, "[pase] schedule: tasks+pending %.3f ms, list-schedule %.3f ms (%lld tasks)\n",
+                     std::chrono::duration<double, std::milli>(tt1 - tt0).count(),
+                     std::chrono::duration<double, std::milli>(tt2 - tt1).count(), (long long)ntk);
     // ---- this rank's tasks in simulated start order
     std::vector<int32_t> mine;
     for (int64_t t = 0; t < ntk; ++t)

@@ -145,46 +145,54 @@ def _ptr(a: np.ndarray, ct):
 
 
 def marshal_graph(graph: dict):
-    """dict -> (pase_graph, keepalive).  Layout per include/pase.h."""
+    """dict -> (pase_graph, keepalive).  Layout per include/pase.h; the node/edge arrays are
+    numpy structured arrays with the ctypes structs' dtype (one vectorised fill per field)."""
     nodes = graph["nodes"]
     edges = graph["edges"]
-    NA = (pase_node * max(len(nodes), 1))()
+    n, m = len(nodes), len(edges)
+    NA = np.zeros(max(n, 1), dtype=np.dtype(pase_node))
+    Z8, Z4 = [0] * PASE_MAX_DIMS, [0] * PASE_MAX_HALO
+    cols = {k: [] for k in ("n_dims", "size", "splittable_mask", "n_out_axes", "out_axes", "n_w_axes",
+                            "w_axes", "flop_dims_mask", "flops_per_point", "n_halo", "halo_spatial",
+                            "halo_filter", "elem_bytes")}
     for v, nd in enumerate(nodes):
         if nd["id"] != v:
             raise ValueError(f"node {v}: id {nd['id']} must equal its index")
-        x = NA[v]
         dims = nd["dims"]
         if len(dims) > PASE_MAX_DIMS:
             raise ValueError(f"node {v}: more than {PASE_MAX_DIMS} dims")
-        x.n_dims = len(dims)
-        for k, d in enumerate(dims):
-            x.size[k] = int(d["size"])
-            if d.get("splittable", True):
-                x.splittable_mask |= 1 << k
-        x.n_out_axes = len(nd["out_axes"])
-        for a, k in enumerate(nd["out_axes"]):
-            x.out_axes[a] = k
-        w = nd.get("w_axes") or []
-        x.n_w_axes = len(w)
-        for a, k in enumerate(w):
-            x.w_axes[a] = k
+        oa = list(nd["out_axes"])
+        w = list(nd.get("w_axes") or [])
         fd = nd.get("flop_dims")
-        x.flop_dims_mask = 0 if fd is None else sum(1 << k for k in fd)
-        x.flops_per_point = int(nd.get("flops_per_point", 2))
         halo = nd.get("halo") or []
         if len(halo) > PASE_MAX_HALO:
             raise ValueError(f"node {v}: more than {PASE_MAX_HALO} halo pairs")
-        x.n_halo = len(halo)
-        for q, (h, f) in enumerate(halo):
-            x.halo_spatial[q], x.halo_filter[q] = h, f
-        x.elem_bytes = int(nd.get("elem_bytes", 4))
-    EA = (pase_edge * max(len(edges), 1))()
-    for e, ed in enumerate(edges):
-        EA[e].src, EA[e].dst = ed["src"], ed["dst"]
-        am = list(ed["axis_map"])
-        for a in range(PASE_MAX_DIMS):
-            EA[e].axis_map[a] = am[a] if a < len(am) else -1
-    g = pase_graph(len(nodes), NA, len(edges), EA)
+        cols["n_dims"].append(len(dims))
+        cols["size"].append([int(d["size"]) for d in dims] + Z8[len(dims):])
+        cols["splittable_mask"].append(sum(1 << k for k, d in enumerate(dims) if d.get("splittable", True)))
+        cols["n_out_axes"].append(len(oa))
+        cols["out_axes"].append(oa + Z8[len(oa):])
+        cols["n_w_axes"].append(len(w))
+        cols["w_axes"].append(w + Z8[len(w):])
+        cols["flop_dims_mask"].append(0 if fd is None else sum(1 << k for k in fd))
+        cols["flops_per_point"].append(int(nd.get("flops_per_point", 2)))
+        cols["n_halo"].append(len(halo))
+        cols["halo_spatial"].append([h for h, _ in halo] + Z4[len(halo):])
+        cols["halo_filter"].append([f for _, f in halo] + Z4[len(halo):])
+        cols["elem_bytes"].append(int(nd.get("elem_bytes", 4)))
+    if n:
+        for k, col in cols.items():
+            if col and isinstance(col[0], list):          # flatten rows: one array conversion
+                NA[k] = np.array([x for row in col for x in row], dtype=NA.dtype[k].base).reshape(n, -1)
+            else:
+                NA[k] = np.array(col, dtype=NA.dtype[k])
+    EA = np.zeros(max(m, 1), dtype=np.dtype(pase_edge))
+    if m:
+        EA["src"] = [ed["src"] for ed in edges]
+        EA["dst"] = [ed["dst"] for ed in edges]
+        EA["axis_map"] = np.array([x for ed in edges for x in list(ed["axis_map"]) + [-1] * (PASE_MAX_DIMS - len(ed["axis_map"]))],
+                                  dtype=np.int32).reshape(m, PASE_MAX_DIMS)
+    g = pase_graph(n, NA.ctypes.data_as(C.POINTER(pase_node)), m, EA.ctypes.data_as(C.POINTER(pase_edge)))
     return g, (NA, EA)
 
 
