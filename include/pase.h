@@ -181,7 +181,8 @@ int64_t pase_table_entries(const pase_ctx* ctx, int32_t rank);
 pase_status pase_set_cost_tables(pase_ctx* ctx, const double* L, const double* W);
 
 /* Persistent-schedule timeline (tracing; enabled by env PASE_TRACE=1 at pase_create): per DP
- * task of the last pase_solve, 4 int64 = {(smid << 32) | rank, t_claim_ns, t_start_ns, t_end_ns}
+ * task of the last pase_solve, 6 int64 = {(smid << 32) | rank, t_claim_ns, t_start_ns (dependencies
+ * met), t_computed_ns (warp 0 done), t_synced_ns (CTA done), t_end_ns (parent counter released)}
  * (%globaltimer).  Copies min(cap, n_tasks) records into out (may be NULL); returns n_tasks
  * (0 when tracing is off, -1 on a CUDA error). */
 int64_t pase_get_trace(const pase_ctx* ctx, int64_t* out, int64_t cap);
@@ -206,8 +207,10 @@ pase_status pase_finish(pase_ctx* ctx, int32_t* configs_out, int32_t* config_ind
 pase_status pase_export_handle(const pase_ctx* ctx, void* blob /* PASE_HANDLE_BYTES */);
 pase_status pase_connect(pase_ctx* ctx, const void* blobs /* world * PASE_HANDLE_BYTES */);
 
-/* Schedule introspection (also on host-only contexts): per DP rank i, vinfo[4i..4i+3] =
- * {partitioned, broadcast flags, this rank's task count, initial pending counter}; tasks =
+/* Schedule introspection (also on host-only contexts): per DP rank i, vinfo[8i..8i+7] =
+ * {partitioned, broadcast flags, this rank's task count, initial pending counter, kernel
+ * shape (-1 generic, 0..63 1-D tile, >= 64 2-D tile), log2 lanes per item group, log2 warps
+ * per item (latency mode), second tiled coordinate (-1 none)}; tasks =
  * this rank's {rank i, first item, end item} triples; order = claim order.  Returns the task
  * count (arrays may be NULL). */
 int64_t pase_get_schedule(const pase_ctx* ctx, int32_t* vinfo, int64_t* tasks, int32_t* order);

@@ -65,7 +65,7 @@ struct pase_ctx {
     int32_t* d_bar = nullptr;               // [0] arrivals, [kSchedLine] epoch, [2 kSchedLine] error
     pase::TaskDesc* d_tasks = nullptr;
     int32_t* d_order = nullptr;
-    int64_t* d_trace = nullptr;             // PASE_TRACE=1: 4 int64 per persistent task
+    int64_t* d_trace = nullptr;             // PASE_TRACE=1: kTraceWords int64 per persistent task
     int ntasks = 0, nblocks = 0;
     int64_t total_tasks = 0;
     bool persistent = true;
@@ -179,9 +179,60 @@ bool trace_on() {
 // lane-group size: each lane should own >= ~8 values of C (K=28 -> 4 lanes, K=84 -> 8,
 // K=205 -> 16, K=456 -> 32): fewer lanes per item amortise the per-item decode and the
 // cross-lane reduction over more candidates.
+bool no_2d() {
+    const char* t = std::getenv("PASE_NO_2D");
+    return t && t[0] == '1';
+}
+
+// 2-D register tile: pick q2 = the coordinate other than qstar (and the
+// multi-GPU partition coordinate) whose first term is latest; use the 2-D tile when its
+// segment structure fits the kernel and it cuts the loads per candidate by >= 20 % on a
+// vertex whose 1-D form is load-heavy.
+void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
+    (void)ctx;
+    if (d.qstar < 0 || d.m < 2 || d.rq < 2) return;
+    // measured (profiles/r01_ab_*.txt): the 1-D tile is faster except with >= 2 suffix
+    // terms, where its per-candidate loads dominate
+    if (d.nterms - d.tstar < 2) return;
+    int q2 = -1, f2 = -1;
+    for (int q = 0; q < d.m; ++q) {
+        if (q == d.qstar || (d.part && q == top) || d.radix[q] < 2) continue;
+        int first = -1;
+        for (int t = 0; t < d.nterms && first < 0; ++t)
+            if (tv[t].stride[q] != 0) first = t;
+        if (first > f2 || (first == f2 && d.radix[q] > d.radix[q2])) { f2 = first; q2 = q; }
+    }
+    if (q2 < 0 || f2 < 1) return;
+    const int nP0 = f2, nP1 = d.tstar - f2, NS = d.nterms - d.tstar;
+    if (nP0 > pase::kMaxP0 || nP1 > pase::kMaxP1 || NS < 1 || NS > 2) return;
+    if (NS == 2 && (tv[d.tstar].stride[q2] != 0 || tv[d.tstar + 1].stride[q2] != 0)) return;
+    for (int t = 0; t < d.nterms; ++t)
+        if (tv[t].stride[q2] >= (int64_t(1) << 31) / 16) return;
+    double l2 = nP0;
+    for (int t = f2; t < d.tstar; ++t) l2 += tv[t].stride[q2] ? pase::kTile2 : 1;
+    for (int t = d.tstar; t < d.nterms; ++t) l2 += tv[t].stride[q2] ? pase::kTile1 * pase::kTile2 : pase::kTile1;
+    const double per2 = l2 / (pase::kTile1 * pase::kTile2);
+    const double per1 = (double)(d.tstar + pase::kTile * NS) / pase::kTile;
+    if (per2 > 0.8 * per1) return;
+    d.q2 = q2;
+    d.rq2 = d.radix[q2];
+    d.t2star = f2;
+    d.ostride_q2 = 1;
+    for (int q = 0; q < q2; ++q) d.ostride_q2 *= d.radix[q];
+    d.ntile2 = (d.rq2 + pase::kTile2 - 1) / pase::kTile2;
+    d.ntile = ((d.rq + pase::kTile1 - 1) / pase::kTile1) * d.ntile2;
+    d.ncombo = d.nout / ((int64_t)d.rq * d.rq2);
+    d.nitems = d.ncombo * d.ntile;
+    d.shape = pase::kShape2D + (NS - 1) * 4 + (d.glog - 2);
+}
+
+// latency mode: vertices with at most this many candidates (N_i * K)
+const int64_t kLatencyCand = std::getenv("PASE_LATENCY_CAND") ? std::atoll(std::getenv("PASE_LATENCY_CAND")) : (1 << 18);
+
 int lane_group_log2(int K) {
+    static const int per_lane = std::getenv("PASE_C_PER_LANE") ? std::atoi(std::getenv("PASE_C_PER_LANE")) : 32;
     int g = 2;
-    while (g < 5 && (1 << (g + 1)) * 8 <= K) ++g;
+    while (g < 5 && (1 << (g + 1)) * per_lane <= K) ++g;
     return g;
 }
 
@@ -348,9 +399,26 @@ pase_status prepare(pase_ctx* ctx, bool device) {
             for (int q = 0; q < d.m; ++q)
                 if (tv[t].stride[q] >= (int64_t(1) << 31) / 16) wide = true;
         const int NP = d.tstar, NS = d.nterms - d.tstar;
+        d.wlog = 0;
+        d.q2 = -1;
+        d.rq2 = 1;
+        d.ntile2 = 1;
+        d.t2star = d.tstar;
+        d.ostride_q2 = 0;
         if (!wide && NP >= 1 && NP <= 4 && NS >= 0 && NS <= 3) {
             d.glog = lane_group_log2(d.K);
+            // latency mode: a small vertex (<= kLatencyCand candidates) is
+            // latency-bound -- on a critical-path chain its few items cannot fill the GPU --
+            // so each item gets L = pow2 >= K/2 lanes (W = L/32 full warps when L > 32): every
+            // lane reduces <= 2 values of C, i.e. one round of loads.
+            if ((int64_t)d.nout * d.K <= kLatencyCand) {
+                int ll = 2;
+                while (ll < 8 && (2 << ll) < d.K) ++ll;
+                d.glog = std::min(ll, 5);
+                d.wlog = ll - d.glog;
+            }
             d.shape = (NP - 1) * 16 + NS * 4 + (d.glog - 2);
+            if (d.wlog == 0 && !no_2d()) try_tile2(ctx, d, tv, top);
         } else {                                          // generic kernel
             d.glog = d.K <= 4 ? 2 : d.K <= 8 ? 3 : d.K <= 16 ? 4 : 5;
             d.shape = -1;
@@ -371,7 +439,7 @@ pase_status prepare(pase_ctx* ctx, bool device) {
         {(void**)&ctx->d_order, sizeof(int32_t) * std::max<size_t>(ctx->sp.order.size(), 1)},
         {(void**)&ctx->d_sched, ctx->sched_bytes},
         {(void**)&ctx->d_bar, sizeof(int32_t) * 3 * pase::kSchedLine},
-        {(void**)&ctx->d_trace, trace_on() ? sizeof(int64_t) * 4 * std::max<size_t>(ctx->sp.tasks.size(), 1) : 0},
+        {(void**)&ctx->d_trace, trace_on() ? sizeof(int64_t) * pase::kTraceWords * std::max<size_t>(ctx->sp.tasks.size(), 1) : 0},
     };
     if ((st = carve(ctx, items2, &ctx->pool2, &ctx->pool2_bytes, device))) return st;
     std::vector<int32_t> sched(sched_words, 0);
@@ -842,10 +910,15 @@ int64_t pase_get_schedule(const pase_ctx* ctx, int32_t* vinfo, int64_t* tasks, i
     const int n = ctx->P.n;
     if (vinfo)
         for (int i = 0; i < n; ++i) {
-            vinfo[4 * i + 0] = ctx->vd[i].part;
-            vinfo[4 * i + 1] = ctx->vd[i].bcast;
-            vinfo[4 * i + 2] = ctx->vd[i].ntasks;
-            vinfo[4 * i + 3] = ctx->sp.pending[i];
+            int32_t* o = vinfo + 8 * i;
+            o[0] = ctx->vd[i].part;
+            o[1] = ctx->vd[i].bcast;
+            o[2] = ctx->vd[i].ntasks;
+            o[3] = ctx->sp.pending[i];
+            o[4] = ctx->vd[i].shape;
+            o[5] = ctx->vd[i].glog;
+            o[6] = ctx->vd[i].wlog;
+            o[7] = ctx->vd[i].q2;
         }
     if (tasks)
         for (size_t t = 0; t < ctx->sp.tasks.size(); ++t) {
@@ -988,7 +1061,7 @@ int64_t pase_get_trace(const pase_ctx* ctx_c, int64_t* out, int64_t cap) {
     pase_ctx* ctx = const_cast<pase_ctx*>(ctx_c);
     if (!ctx || ctx->dev < 0 || !ctx->d_trace || !trace_on()) return 0;
     const int64_t nt = std::min<int64_t>(ctx->ntasks, cap);
-    if (out && nt > 0 && cudaMemcpy(out, ctx->d_trace, sizeof(int64_t) * 4 * nt, cudaMemcpyDeviceToHost) != cudaSuccess)
+    if (out && nt > 0 && cudaMemcpy(out, ctx->d_trace, sizeof(int64_t) * pase::kTraceWords * nt, cudaMemcpyDeviceToHost) != cudaSuccess)
         return -1;
     return ctx->ntasks;
 }

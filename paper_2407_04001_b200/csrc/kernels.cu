@@ -193,23 +193,33 @@ __device__ __forceinline__ void st_out(const VertexDesc& vd, int64_t phi, double
         }
 }
 
-// Items [first + k*stride + sub, ...) < end for the calling warp (warp-uniform loop).
+// Items of [i0, i1) for the calling warp.  Throughput mode (wlog == 0): the warp's lane
+// groups take items first + k*stride + sub (warp-uniform loop).  Latency mode (G == 32,
+// W = 2^wlog warps per item, for small vertices on the critical path): the W warps of an item
+// split its C range (one round of loads per lane instead of K / (2G)), and their partial
+// minima are combined through shared memory (CTA-uniform loop, CTA barriers).
 template <int NP, int NS, int G>
 __device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td, int64_t first,
-                                        int64_t stride, int64_t end) {
+                                        int64_t stride, int64_t i1, double* red_b, int* red_c) {
     constexpr int V = kTile;
     constexpr int LG = Log2<G>::value, LV = Log2<V>::value;
     constexpr int S = LG < LV ? LG : LV;          // halving (reduce-scatter) steps
     constexpr int H = V >> S;                     // values a lane holds afterwards
     const int lane = threadIdx.x & (G - 1);
-    const int sub = (threadIdx.x & 31) / G;
+    const int wlog = G == 32 ? vd.wlog : 0;
+    const int wsub = (threadIdx.x >> 5) & ((1 << wlog) - 1);      // warp's slice of C
+    const int sub = wlog ? 0 : (threadIdx.x & 31) / G;
     const int q = vd.qstar;
     int sq[NS > 0 ? NS : 1];                            // host guarantees strides < 2^31
 #pragma unroll
     for (int t = 0; t < NS; ++t) sq[t] = (int)td[NP + t].stride[q];
+    // latency mode: rounds start at the CTA's first slot so every warp runs the same count
+    const int64_t wib = (threadIdx.x >> 5) >> wlog;                // item slot within the CTA
+    const int64_t b0 = wlog ? first - wib : first;
+    const int64_t end = i1;
 
-    for (int64_t base = first; base < end; base += stride) {
-        const int64_t item = base + sub;
+    for (int64_t base = b0; base < end; base += stride) {
+        const int64_t item = wlog ? base + wib : base + sub;
         const bool valid = item < end;
         const uint32_t it = valid ? (uint32_t)item : 0u;   // host guarantees nitems < 2^31
         const uint32_t nc = (uint32_t)vd.ncombo;
@@ -242,8 +252,9 @@ __device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td
         for (int j = 0; j < V; ++j) { best[j] = __longlong_as_double(0x7ff0000000000000ll); bestC[j] = 0x7fffffff; }
         const int Kv = nb > 0 ? vd.K : 0;
         const int jmax = nb > 0 ? nb - 1 : 0;
+        const int cstep = G << wlog;
 #pragma unroll 2
-        for (int C = lane; C < Kv; C += G) {                // unrolled: loads of 2 C in flight
+        for (int C = lane + (wsub << LG); C < Kv; C += cstep) {   // unrolled: 2 C in flight
             double pre = ld(pp[0] + C);                     // L[C] (term 0 is never in the suffix)
 #pragma unroll
             for (int t = 1; t < NP; ++t) pre = __dadd_rn(pre, ld(pp[t] + C));
@@ -287,11 +298,196 @@ __device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td
 #pragma unroll
         for (int s = 0; s < S; ++s)
             if (lane & (G >> (s + 1))) jbase += V >> (s + 1);
-        if ((lane & ((G >> S) - 1)) == 0) {
+        if (G == 32 && wlog) {                              // combine the W warps' partials
+            const int w = threadIdx.x >> 5;
+            if ((lane & ((G >> S) - 1)) == 0)
+#pragma unroll
+                for (int k = 0; k < H; ++k) {
+                    red_b[w * V + jbase + k] = best[k];
+                    red_c[w * V + jbase + k] = bestC[k];
+                }
+            __syncthreads();
+            if (wsub == 0 && lane < V) {
+                double b = red_b[w * V + lane];
+                int c = red_c[w * V + lane];
+                for (int k = 1; k < (1 << wlog); ++k) combine(b, c, red_b[(w + k) * V + lane], red_c[(w + k) * V + lane]);
+                if (lane < nb) st_out(vd, obase + (int64_t)(x0 + lane) * vd.ostride_q, b, c);
+            }
+            __syncthreads();
+        } else if ((lane & ((G >> S) - 1)) == 0) {
 #pragma unroll
             for (int k = 0; k < H; ++k) {
                 const int j = jbase + k;
                 if (j < nb) st_out(vd, obase + (int64_t)(x0 + j) * vd.ostride_q, best[k], bestC[k]);
+            }
+        }
+    }
+}
+
+// 2-D register tile: a work item is one combination of the D(i) coordinates
+// other than (qstar, q2) times a kTile1 x kTile2 block of (qstar, q2) values.  Per C, the
+// canonical sum is built in its own order with loop-invariant prefixes hoisted:
+//   pre      = terms [0, t2star)            (scalar: depend on neither tiled coordinate)
+//   p1[j2]   = pre + terms [t2star, tstar)  (depend on q2 at most: kTile2 partials)
+//   cost     = p1[j2] + S terms             (S = [tstar, nterms): kTile1 x kTile2 candidates)
+// so per C a lane loads t2star + (kTile2 or 1 per P1 term) + (kTile1 or kTile1*kTile2 per S
+// term) values for 16 candidates instead of NP + 8 NS for 8 (1-D tile).  Association order
+// is unchanged, so the results are bit-identical to the oracle's.  NS = 1 (S term on qstar,
+// optionally also q2) or NS = 2 (both S terms on qstar only).
+template <int NS, int G>
+__device__ __noinline__ void tile2_items(const VertexDesc& vd, const TermDesc* td, int64_t first,
+                                         int64_t stride, int64_t end) {
+    constexpr int V1 = kTile1, V2 = kTile2, V = V1 * V2;
+    constexpr int LG = Log2<G>::value, LV = Log2<V>::value;
+    constexpr int S = LG < LV ? LG : LV;
+    constexpr int H = V >> S;
+    const int lane = threadIdx.x & (G - 1);
+    const int sub = (threadIdx.x & 31) / G;
+    const int q1 = vd.qstar, q2 = vd.q2;
+    const int nP0 = vd.t2star, nP1 = vd.tstar - vd.t2star, ts = vd.tstar;
+    // per-term strides along the tiled coordinates (host: < 2^31)
+    int p1s[kMaxP1];
+#pragma unroll
+    for (int t = 0; t < kMaxP1; ++t) p1s[t] = t < nP1 ? (int)td[nP0 + t].stride[q2] : 0;
+    int s1[NS], s2[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) { s1[t] = (int)td[ts + t].stride[q1]; s2[t] = (int)td[ts + t].stride[q2]; }
+
+    for (int64_t base = first; base < end; base += stride) {
+        const int64_t item = base + sub;
+        const bool valid = item < end;
+        const uint32_t it = valid ? (uint32_t)item : 0u;
+        const uint32_t nc = (uint32_t)vd.ncombo;
+        uint32_t rem = it % nc;
+        const uint32_t tidx = it / nc;
+        const int x2 = (int)(tidx % (uint32_t)vd.ntile2) * V2;
+        const int x1 = (int)(tidx / (uint32_t)vd.ntile2) * V1;
+        const int nb1 = valid ? min(V1, vd.rq - x1) : 0;
+        const int nb2 = valid ? min(V2, vd.rq2 - x2) : 0;
+        const double* pp[kMaxP0];
+        const double* pq[kMaxP1];
+        const double* ps[NS];
+#pragma unroll
+        for (int t = 0; t < kMaxP0; ++t) pp[t] = td[t < nP0 ? t : 0].base;
+#pragma unroll
+        for (int t = 0; t < kMaxP1; ++t) pq[t] = t < nP1 ? td[nP0 + t].base + (int64_t)x2 * p1s[t] : pp[0];
+#pragma unroll
+        for (int t = 0; t < NS; ++t) ps[t] = td[ts + t].base + (int64_t)x1 * s1[t] + (int64_t)x2 * s2[t];
+        int64_t obase = 0, ost = 1;
+        for (int c = 0; c < vd.m; ++c) {                    // mixed-radix decode (lowest fastest)
+            const uint32_t r = (uint32_t)vd.radix[c];
+            if (c != q1 && c != q2) {
+                const uint32_t v = rem % r;
+                rem /= r;
+                obase += (int64_t)v * ost;
+#pragma unroll
+                for (int t = 0; t < kMaxP0; ++t) if (t < nP0) pp[t] += (int64_t)v * td[t].stride[c];
+#pragma unroll
+                for (int t = 0; t < kMaxP1; ++t) if (t < nP1) pq[t] += (int64_t)v * td[nP0 + t].stride[c];
+#pragma unroll
+                for (int t = 0; t < NS; ++t) ps[t] += (int64_t)v * td[ts + t].stride[c];
+            }
+            ost *= r;
+        }
+        double best[V];
+        int bestC[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) { best[j] = __longlong_as_double(0x7ff0000000000000ll); bestC[j] = 0x7fffffff; }
+        const int Kv = (nb1 > 0 && nb2 > 0) ? vd.K : 0;
+        const int m1 = nb1 > 0 ? nb1 - 1 : 0, m2 = nb2 > 0 ? nb2 - 1 : 0;
+        // every load of an iteration is unconditional (unused slots re-read a valid address), so
+        // they issue together; only the adds are predicated on the vertex's segment sizes
+#pragma unroll 1
+        for (int C = lane; C < Kv; C += G) {
+            double a[kMaxP0];
+#pragma unroll
+            for (int t = 0; t < kMaxP0; ++t) a[t] = ld(pp[t] + C);
+            double b[kMaxP1][V2];
+#pragma unroll
+            for (int t = 0; t < kMaxP1; ++t)
+#pragma unroll
+                for (int j2 = 0; j2 < V2; ++j2) b[t][j2] = ld(pq[t] + (int64_t)min(j2, m2) * p1s[t] + C);
+            double pre = a[0];
+#pragma unroll
+            for (int t = 1; t < kMaxP0; ++t) if (t < nP0) pre = __dadd_rn(pre, a[t]);
+            double p1[V2];
+#pragma unroll
+            for (int j2 = 0; j2 < V2; ++j2) {
+                p1[j2] = pre;
+#pragma unroll
+                for (int t = 0; t < kMaxP1; ++t) if (t < nP1) p1[j2] = __dadd_rn(p1[j2], b[t][j2]);
+            }
+            if (NS == 1 && s2[0] != 0) {                    // S term on (qstar, q2)
+                double x[V1][V2];
+#pragma unroll
+                for (int j1 = 0; j1 < V1; ++j1)
+#pragma unroll
+                    for (int j2 = 0; j2 < V2; ++j2)
+                        x[j1][j2] = ld(ps[0] + (int64_t)min(j1, m1) * s1[0] + (int64_t)min(j2, m2) * s2[0] + C);
+#pragma unroll
+                for (int j1 = 0; j1 < V1; ++j1)
+#pragma unroll
+                    for (int j2 = 0; j2 < V2; ++j2) {
+                        const double cost = __dadd_rn(p1[j2], x[j1][j2]);
+                        const int j = j1 * V2 + j2;
+                        if (cost < best[j]) { best[j] = cost; bestC[j] = C; }
+                    }
+            } else {                                        // S terms on qstar only
+                double x[NS][V1];
+#pragma unroll
+                for (int t = 0; t < NS; ++t)
+#pragma unroll
+                    for (int j1 = 0; j1 < V1; ++j1) x[t][j1] = ld(ps[t] + (int64_t)min(j1, m1) * s1[t] + C);
+#pragma unroll
+                for (int j1 = 0; j1 < V1; ++j1)
+#pragma unroll
+                    for (int j2 = 0; j2 < V2; ++j2) {
+                        double cost = __dadd_rn(p1[j2], x[0][j1]);
+#pragma unroll
+                        for (int t = 1; t < NS; ++t) cost = __dadd_rn(cost, x[t][j1]);
+                        const int j = j1 * V2 + j2;
+                        if (cost < best[j]) { best[j] = cost; bestC[j] = C; }
+                    }
+            }
+        }
+        // butterfly reduce-scatter across the G lanes of the group (as tile_items)
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int o = G >> (s + 1);
+            const int half = V >> (s + 1);
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int k = 0; k < half; ++k) {
+                const double sb = up ? best[k] : best[k + half];
+                const int sc = up ? bestC[k] : bestC[k + half];
+                double kb = up ? best[k + half] : best[k];
+                int kc = up ? bestC[k + half] : bestC[k];
+                const double rb = __shfl_xor_sync(0xffffffffu, sb, o);
+                const int rc = __shfl_xor_sync(0xffffffffu, sc, o);
+                combine(kb, kc, rb, rc);
+                best[k] = kb;
+                bestC[k] = kc;
+            }
+        }
+#pragma unroll
+        for (int o = G >> (S + 1); o >= 1; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+                const double rb = __shfl_xor_sync(0xffffffffu, best[k], o);
+                const int rc = __shfl_xor_sync(0xffffffffu, bestC[k], o);
+                combine(best[k], bestC[k], rb, rc);
+            }
+        int jbase = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (lane & (G >> (s + 1))) jbase += V >> (s + 1);
+        if ((lane & ((G >> S) - 1)) == 0) {
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+                const int j = jbase + k, j1 = j / V2, j2 = j % V2;
+                if (j1 < nb1 && j2 < nb2)
+                    st_out(vd, obase + (int64_t)(x1 + j1) * vd.ostride_q + (int64_t)(x2 + j2) * vd.ostride_q2,
+                           best[k], bestC[k]);
             }
         }
     }
@@ -333,14 +529,20 @@ __device__ __noinline__ void generic_items(const VertexDesc& vd, const TermDesc*
 }
 
 // shape index: 0..63 = tiled (NP-1)*16 + NS*4 + (log2 G - 2); -1 = generic
+//   first_warp / nwarps: the calling warp's index / the warps sharing [i0, i1) (a CTA's warps
+//   are consecutive).  Item slots per warp: 32/G (throughput mode) or 1/W (latency mode).
 __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const TermDesc* td_sh,
                                           const TermDesc* tds_g, int64_t first_warp, int64_t nwarps,
-                                          int64_t i0, int64_t i1) {
+                                          int64_t i0, int64_t i1, double* red_b, int* red_c) {
     switch (shape) {
 #define PASE_CASE(NP, NS, LGG)                                                                    \
     case (NP - 1) * 16 + NS * 4 + (LGG - 2): {                                                    \
         constexpr int G_ = 1 << LGG, GPW_ = 32 / G_;                                              \
-        tile_items<NP, NS, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1);             \
+        if (G_ == 32 && vd.wlog)                                                                  \
+            tile_items<NP, NS, G_>(vd, td_sh, i0 + (first_warp >> vd.wlog), nwarps >> vd.wlog, i1,   \
+                                   red_b, red_c);                                                 \
+        else                                                                                      \
+            tile_items<NP, NS, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1, red_b, red_c); \
         return;                                                                                   \
     }
 #define PASE_NS(NP, NS) PASE_CASE(NP, NS, 2) PASE_CASE(NP, NS, 3) PASE_CASE(NP, NS, 4) PASE_CASE(NP, NS, 5)
@@ -349,6 +551,15 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
 #undef PASE_NP
 #undef PASE_NS
 #undef PASE_CASE
+#define PASE_CASE2(NS, LGG)                                                                       \
+    case kShape2D + (NS - 1) * 4 + (LGG - 2): {                                                   \
+        constexpr int G_ = 1 << LGG, GPW_ = 32 / G_;                                              \
+        tile2_items<NS, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1);                \
+        return;                                                                                   \
+    }
+        PASE_CASE2(1, 2) PASE_CASE2(1, 3) PASE_CASE2(1, 4) PASE_CASE2(1, 5)
+        PASE_CASE2(2, 2) PASE_CASE2(2, 3) PASE_CASE2(2, 4) PASE_CASE2(2, 5)
+#undef PASE_CASE2
         default: {
             const int gpw = 32 >> vd.glog;
             generic_items(vd, tds_g, vd.glog, i0 + first_warp * gpw, nwarps * gpw, i1);
@@ -361,13 +572,15 @@ __global__ void __launch_bounds__(256, 2)
 dp_fill_vertex(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ tds, int vtx) {
     __shared__ VertexDesc vd;
     __shared__ TermDesc td[kMaxTermsSh];
+    __shared__ double red_b[8 * kTile];
+    __shared__ int red_c[8 * kTile];
     if (threadIdx.x == 0) vd = vds[vtx];
     const int nt = min(vds[vtx].nterms, kMaxTermsSh);
     for (int t = threadIdx.x; t < nt; t += blockDim.x) td[t] = tds[vds[vtx].term0 + t];
     __syncthreads();
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    run_shape(vd.shape, vd, td, tds, warp, nwarps, 0, vd.shape >= 0 ? vd.nitems : vd.nout);
+    run_shape(vd.shape, vd, td, tds, warp, nwarps, 0, vd.shape >= 0 ? vd.nitems : vd.nout, red_b, red_c);
 }
 
 void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vertex,
@@ -375,7 +588,7 @@ void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vert
     const int threads = 256;
     const int G = 1 << vh.glog;
     const int64_t units = vh.shape >= 0 ? vh.nitems : vh.nout;
-    int64_t blocks = (units * G + threads - 1) / threads;
+    int64_t blocks = ((units * G << vh.wlog) + threads - 1) / threads;
     blocks = blocks > 148 * 8 ? 148 * 8 : (blocks < 1 ? 1 : blocks);
     dp_fill_vertex<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(vd_dev, td_dev, vertex);
 }
@@ -443,6 +656,8 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
     const bool multi = peers.world > 1;                     // peers: .sys scope
     __shared__ VertexDesc vd;
     __shared__ TermDesc td[kMaxTermsSh];
+    __shared__ double red_b[8 * kTile];                     // latency-mode partial minima
+    __shared__ int red_c[8 * kTile];
     __shared__ int s_task;
     const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     int cur = -1;
@@ -482,9 +697,12 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
         __syncthreads();
         task = s_task;
         if (task < 0) break;                                // timed out (reported via *err)
-        run_shape(vd.shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1);
+        run_shape(vd.shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1, red_b, red_c);
+        int64_t t_comp = 0, t_sync = 0;
+        if (trace && threadIdx.x == 0) t_comp = (int64_t)globaltimer();
         __syncthreads();                                    // task's stores precede the release
         if (threadIdx.x == 0) {
+            if (trace) t_sync = (int64_t)globaltimer();
             if (vd.parent >= 0) {
                 if (vd.bcast & 1) {                         // every rank's copy of the parent waits
                     for (int q = 0; q < peers.world; ++q) red_add_release_sys(peers.pending[q] + vd.parent, -1);
@@ -495,10 +713,13 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
                 }
             }
             if (trace) {                                    // PASE_TRACE: per-task timeline
-                trace[4 * task + 0] = ((int64_t)smid() << 32) | (uint32_t)tk.vtx;
-                trace[4 * task + 1] = t_claim;
-                trace[4 * task + 2] = t_start;
-                trace[4 * task + 3] = (int64_t)globaltimer();
+                int64_t* tr = trace + (int64_t)kTraceWords * task;
+                tr[0] = ((int64_t)smid() << 32) | (uint32_t)tk.vtx;
+                tr[1] = t_claim;
+                tr[2] = t_start;
+                tr[3] = t_comp;
+                tr[4] = t_sync;
+                tr[5] = (int64_t)globaltimer();
             }
         }
     }

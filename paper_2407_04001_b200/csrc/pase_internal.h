@@ -93,7 +93,17 @@ struct VertexDesc {          // one DP vertex (rank i)
     int64_t ostride_q;       // output stride of qstar
     int64_t ncombo;          // nout / rq
     int64_t nitems;          // ncombo * ntile
+    // 2-D register tile (shape >= kShape2D): a kTile1 x kTile2 block of outputs
+    // along (qstar, q2).  Terms [0, t2star) depend on neither (scalar prefix), [t2star, tstar)
+    // on q2 at most, [tstar, nterms) on qstar and maybe q2.  ntile = ntile1 * ntile2 and
+    // ncombo = nout / (rq * rq2) then; item = combo + ncombo * (t2 + ntile2 * t1).
+    int32_t q2;              // second tiled coordinate (-1: 1-D tiling)
+    int32_t rq2;             // its radix
+    int32_t ntile2;          // tiles along q2
+    int32_t t2star;          // first term depending on q2
+    int64_t ostride_q2;      // output stride of q2
     int32_t glog;            // log2 lane-group size
+    int32_t wlog;            // log2 warps per item (latency mode, glog == 5 only)
     int32_t shape;           // tiled variant (NP-1)*16 + NS*4 + (glog-2), or -1 = generic kernel
     int32_t ntasks;          // persistent schedule: this rank's tasks of the vertex ...
     int32_t task0;           // ... with local ids [task0, task0 + ntasks)
@@ -118,6 +128,7 @@ struct Peers {               // kernel parameter: the group's scheduler words (d
     int32_t world, rank;
 };
 
+constexpr int kTraceWords = 6;                // PASE_TRACE record per task (pase_get_trace)
 constexpr int kTasksPerBlock = 4;   // big vertices: ~4 tasks per CTA of the grid
 
 struct SchedPlan {           // build_schedule output for one rank
@@ -132,6 +143,9 @@ struct SchedPlan {           // build_schedule output for one rank
 pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world, int rank, int nblocks,
                            SchedPlan& out, std::string& err);
 constexpr int kTile = 8;     // max outputs per lane group along qstar
+constexpr int kTile1 = 4, kTile2 = 4;   // 2-D tile: outputs along qstar x q2
+constexpr int kShape2D = 64;            // shapes >= kShape2D: 2-D tiled (NS-1)*4 + (glog-2)
+constexpr int kMaxP0 = 4, kMaxP1 = 2;   // 2-D tile: max scalar-prefix / q2-prefix terms
 constexpr int kCostRows = 64;  // edge-table rows per cost-table CTA
 
 struct BtDesc {               // back-substitution record of one rank, in back-level order

@@ -41,7 +41,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     for (int i = 0; i < n; ++i) {
         const VertexDesc& d = vd[i];
         const int64_t units = d.shape >= 0 ? d.nitems : d.nout;
-        const int64_t groups = 256 >> d.glog;
+        const int64_t groups = (256 >> d.glog) >> d.wlog;   // items a CTA runs concurrently
         for (int q = 0; q < G; ++q) {
             std::vector<std::pair<int64_t, int64_t>> runs;
             if (!d.part) {
@@ -108,7 +108,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     std::vector<double> tdur(ntk), bl(n, 0.0);
     for (int64_t t = 0; t < ntk; ++t) {
         const VertexDesc& d = vd[all[t].vtx];
-        const double cand = (double)(all[t].i1 - all[t].i0) * d.K * (d.shape >= 0 ? kTile : 1);
+        const double cand = (double)(all[t].i1 - all[t].i0) * d.K * (d.shape < 0 ? 1 : d.q2 >= 0 ? kTile1 * kTile2 : kTile);
         tdur[t] = 3.0 + cand / 3000.0;
     }
     for (int i = n - 1; i >= 0; --i) {                 // parents have higher ranks

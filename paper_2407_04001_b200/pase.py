@@ -20,6 +20,7 @@ PASE_MAX_DIMS = 8
 PASE_MAX_HALO = 4
 PASE_MAX_DEP = 12
 PASE_HANDLE_BYTES = 256
+TRACE_WORDS = 6
 PASE_CFG_EXACT_P, PASE_CFG_LE_P = 0, 1
 STATUS = {0: "PASE_OK", 1: "PASE_ERR_INVALID", 2: "PASE_ERR_RESOURCE", 3: "PASE_ERR_CUDA",
           4: "PASE_ERR_NCCL", 5: "PASE_ERR_STATE"}
@@ -293,9 +294,10 @@ class Context:
         self._chk(self._L.pase_connect(self._h, buf))
 
     def schedule(self) -> Dict[str, np.ndarray]:
-        """pase_get_schedule: per-vertex (part, bcast, ntasks, pending), tasks, claim order."""
+        """pase_get_schedule: per-vertex (part, bcast, ntasks, pending, shape, glog, wlog, q2),
+        tasks, claim order."""
         nt = self._L.pase_get_schedule(self._h, None, None, None)
-        vinfo = np.zeros((self.n, 4), np.int32)
+        vinfo = np.zeros((self.n, 8), np.int32)
         tasks = np.zeros((max(nt, 1), 3), np.int64)
         order = np.zeros(max(nt, 1), np.int32)
         self._L.pase_get_schedule(self._h, _ptr(vinfo, C.c_int32), _ptr(tasks, C.c_int64), _ptr(order, C.c_int32))
@@ -356,14 +358,15 @@ class Context:
         return T, A
 
     def trace(self) -> np.ndarray:
-        """PASE_TRACE=1 timeline of the last solve: rows (rank, smid, t_claim, t_start, t_end) ns."""
+        """PASE_TRACE=1 timeline of the last solve, one row per DP task (ns, %globaltimer):
+        (rank, smid, t_claim, t_start, t_computed, t_synced, t_end)."""
         n = self._L.pase_get_trace(self._h, None, 0)
         if n <= 0:
-            return np.zeros((0, 5), np.int64)
-        buf = np.zeros(4 * n, np.int64)
+            return np.zeros((0, 7), np.int64)
+        buf = np.zeros(TRACE_WORDS * n, np.int64)
         self._L.pase_get_trace(self._h, _ptr(buf, C.c_int64), n)
-        r = buf.reshape(n, 4)
-        out = np.zeros((n, 5), np.int64)
+        r = buf.reshape(n, TRACE_WORDS)
+        out = np.zeros((n, 7), np.int64)
         out[:, 0] = r[:, 0] & 0xffffffff
         out[:, 1] = r[:, 0] >> 32
         out[:, 2:] = r[:, 1:]

@@ -31,9 +31,10 @@ KEYS = [
 out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 h = rows[0]
+units = dict(zip(h, rows[1]))
 for r in rows[2:]:
     d = dict(zip(h, r))
     print("kernel:", d.get("Kernel Name", "")[:90])
     for k, lab in KEYS:
         if k in d:
-            print(f"  {lab:16s} {d[k]}")
+            print(f"  {lab:16s} {d[k]} {units.get(k, '')}")

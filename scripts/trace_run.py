@@ -38,7 +38,7 @@ st = ctx.stats()
 os.makedirs("gpurun_out", exist_ok=True)
 np.save(f"gpurun_out/trace_{wl}.npy", tr)
 t0 = tr[:, 2].min()
-print(f"dp phase {st['ms_dp']:.3f} ms, tasks {len(tr)}, span {(tr[:, 4].max() - t0) / 1e3:.1f} us")
+print(f"dp phase {st['ms_dp']:.3f} ms, tasks {len(tr)}, span {(tr[:, 6].max() - t0) / 1e3:.1f} us")
 n = len(sigma)
 rows = []
 for i in range(n):
@@ -46,8 +46,8 @@ for i in range(n):
     if not m.any():
         continue
     cand = int(K[sigma[i]]) * math.prod(int(K[u]) for u in deps[i])
-    s, e = tr[m, 3].min() - t0, tr[m, 4].max() - t0
-    busy = (tr[m, 4] - tr[m, 3]).sum()
+    s, e = tr[m, 3].min() - t0, tr[m, 6].max() - t0
+    busy = (tr[m, 6] - tr[m, 3]).sum()
     waitw = (tr[m, 3] - tr[m, 2]).sum()
     rows.append((i, int(m.sum()), cand, s / 1e3, e / 1e3, (e - s) / 1e3, busy / 1e3, waitw / 1e3))
 rows.sort(key=lambda r: -r[5])
