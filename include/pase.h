@@ -190,6 +190,26 @@ int64_t pase_get_trace(const pase_ctx* ctx, int64_t* out, int64_t cap);
 /* Time the solve phases separately on the next pase_solve (adds syncs; default off). */
 pase_status pase_set_profiling(pase_ctx* ctx, int32_t enable);
 
+/* ---- Eq. 1 on the GPU (eval.cu) -------------------------------------------
+ * Both use the context's cost tables: the cost-table kernel's L_v / W_e (recomputed by the
+ * call on the context's stream), or the tables given to pase_set_cost_tables.  The sum is Eq. 1
+ * written out in one fixed order: 0 + L_v[phi(v)] over node ids, then + W_e over
+ * edge ids, each an IEEE round-to-nearest add.  Synchronous (return after the device work).
+ * Multi-GPU contexts evaluate on their own device only (no group call). */
+
+/* cost(G, phi) for n_strategies strategies: config_index = int32[n_strategies * n_nodes]
+ * (row s = strategy s, entry v = index of phi(v) in C(v)); cost_out = double[n_strategies].
+ * PASE_ERR_INVALID names the first index outside [0, K_v). */
+pase_status pase_evaluate(pase_ctx* ctx, const int32_t* config_index, int64_t n_strategies, double* cost_out);
+
+/* Exhaustive search: the minimum of Eq. 1 over all prod_v K_v strategies, which
+ * Theorem 1 says equals pase_solve's total.  Strategy index = mixed radix over
+ * node ids, node 0 fastest; among equal costs the lowest index wins.  max_strategies = 0
+ * means 2^40; a larger space returns PASE_ERR_RESOURCE.  Outputs (each may be NULL):
+ * config_index_out = int32[n_nodes], total_cost_out, n_strategies_out = prod_v K_v. */
+pase_status pase_brute_force(pase_ctx* ctx, uint64_t max_strategies, int32_t* config_index_out,
+                             double* total_cost_out, uint64_t* n_strategies_out);
+
 /* ---- split solve (a multi-GPU group launches every rank before waiting on any) ---------- */
 pase_status pase_launch(pase_ctx* ctx);       /* enqueue one solve on the context's stream */
 pase_status pase_finish(pase_ctx* ctx, int32_t* configs_out, int32_t* config_index_out,

@@ -56,13 +56,14 @@ struct pase_ctx {
     int nbtlev = 0;
     int32_t* d_choice = nullptr;
     double* d_total = nullptr;
+    int32_t* d_err = nullptr;               // scheduler time-out flag (inside the output block)
     // pool 2: scheduler (pending counters written by peers), tasks, claim order, trace
     void* pool2 = nullptr;
     size_t pool2_bytes = 0;
     int32_t* d_sched = nullptr;             // [0] claim counter | [kSchedLine, +n) pending
     int32_t* d_sched_init = nullptr;        // its solve-start image
     size_t sched_bytes = 0;
-    int32_t* d_bar = nullptr;               // [0] arrivals, [kSchedLine] epoch, [2 kSchedLine] error
+    int32_t* d_bar = nullptr;               // [0] arrivals, [kSchedLine] epoch
     pase::TaskDesc* d_tasks = nullptr;
     int32_t* d_order = nullptr;
     int64_t* d_trace = nullptr;             // PASE_TRACE=1: kTraceWords int64 per persistent task
@@ -289,8 +290,9 @@ pase_status allocate(pase_ctx* ctx, bool device) {
         {(void**)&ctx->d_W, sizeof(double) * std::max<int64_t>(P.woff[m], 1)},
         {(void**)&ctx->d_T, sizeof(double) * P.toff[n]},
         {(void**)&ctx->d_A, sizeof(uint16_t) * P.toff[n]},
-        {(void**)&ctx->d_choice, sizeof(int32_t) * n},
-        {(void**)&ctx->d_total, sizeof(double)},
+        // solve outputs, laid out as the pinned host block: total | err | pad | choice[n]
+        // (one D2H copy per solve)
+        {(void**)&ctx->d_total, 16 + sizeof(int32_t) * n},
     };
     size_t total = 0;
     for (auto& it : items) total += align_up(it.bytes);
@@ -303,7 +305,10 @@ pase_status allocate(pase_ctx* ctx, bool device) {
         ctx->err = buf;
         return PASE_ERR_RESOURCE;
     }
-    return carve(ctx, items, &ctx->pool, &ctx->pool_bytes, device);
+    pase_status st = carve(ctx, items, &ctx->pool, &ctx->pool_bytes, device);
+    ctx->d_err = (int32_t*)((char*)ctx->d_total + 8);
+    ctx->d_choice = (int32_t*)((char*)ctx->d_total + 16);
+    return st;
 }
 
 // Vertex/term descriptors, the task schedule (schedule.cpp), pool 2, upload.
@@ -410,7 +415,10 @@ pase_status prepare(pase_ctx* ctx, bool device) {
             // latency mode: a small vertex (<= kLatencyCand candidates) is
             // latency-bound -- on a critical-path chain its few items cannot fill the GPU --
             // so each item gets L = pow2 >= K/2 lanes (W = L/32 full warps when L > 32): every
-            // lane reduces <= 2 values of C, i.e. one round of loads.
+            // lane reduces <= 2 values of C, i.e. one round of loads.  (Measured: widening the
+            // lane groups of mid-size vertices too -- up to a warp, or to K/2 lanes, whenever
+            // their items cannot fill the grid -- is slower overall: 0.58 -> 0.76 / 1.42 ms DP
+            // on Transformer p=64; the extra tasks cost more than the shorter chains save.)
             if ((int64_t)d.nout * d.K <= kLatencyCand) {
                 int ll = 2;
                 while (ll < 8 && (2 << ll) < d.K) ++ll;
@@ -528,7 +536,7 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
     cudaStream_t s = ctx->stream;
     if (capture) CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     const unsigned ext = capture ? cudaEventRecordExternal : cudaEventRecordDefault;
-    int32_t* d_err = ctx->d_bar + 2 * pase::kSchedLine;
+    int32_t* d_err = ctx->d_err;
     CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int32_t), s));
     if (!ctx->override_tables)
         pase::launch_cost_tables(ctx->d_nodes, ctx->d_K, ctx->d_cfg_off, ctx->d_cfg, ctx->d_loff, n,
@@ -564,9 +572,7 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
     CUDA_TRY(cudaEventRecordWithFlags(ctx->ev_dp, s, ext));
     pase::launch_backtrack(ctx->d_bt, ctx->d_bt_off, ctx->nbtlev, n, ctx->vd[n - 1].T, ctx->d_choice,
                            ctx->d_total, s);
-    CUDA_TRY(cudaMemcpyAsync(ctx->h_choice, ctx->d_choice, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->h_total, ctx->d_total, sizeof(double), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(ctx->h_err, d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_total, ctx->d_total, 16 + sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
     cudaError_t ce = cudaSuccess;
     cudaGraph_t graph = nullptr;
     if (capture) ce = cudaStreamEndCapture(s, &graph);
@@ -628,7 +634,7 @@ void fill_stats(pase_ctx* ctx) {
     s.alg_bytes_tables = 8ull * s.cost_entries;
     s.comm_bytes = comm;
     s.h2d_bytes = ctx->h2d_bytes;
-    s.d2h_bytes = sizeof(int32_t) * P.n + sizeof(double) + sizeof(int32_t);
+    s.d2h_bytes = 16 + sizeof(int32_t) * P.n;     // one copy: total | err | pad | choice[n]
 }
 
 // Group handle blob (PASE_HANDLE_BYTES): how a peer reaches this context's pools.
@@ -1069,6 +1075,126 @@ int64_t pase_get_trace(const pase_ctx* ctx_c, int64_t* out, int64_t cap) {
 pase_status pase_set_profiling(pase_ctx* ctx, int32_t enable) {
     if (!ctx) return PASE_ERR_INVALID;
     ctx->profiling = enable;
+    return PASE_OK;
+}
+
+// ---- row f2: Eq. 1 on the GPU (eval.cu) ----------------------------------------------------
+namespace {
+// The cost tables the Eq. 1 kernels read: the cost-table kernel's output (recomputed on the
+// context's stream) unless pase_set_cost_tables replaced them.  Also uploads the W_e index
+// records (row = later endpoint: the DP layout) into a stream-ordered temporary.
+pase_status eq1_prepare(pase_ctx* ctx, pase::EvalEdge** ed_dev) {
+    const Plan& P = ctx->P;
+    CUDA_TRY(cudaSetDevice(ctx->dev));
+    if (!ctx->override_tables)
+        pase::launch_cost_tables(ctx->d_nodes, ctx->d_K, ctx->d_cfg_off, ctx->d_cfg, ctx->d_loff, P.n,
+                                 ctx->d_edges, ctx->d_chunks, ctx->nchunks, P.r, ctx->d_L, ctx->d_W, ctx->stream);
+    std::vector<pase::EvalEdge> ed(std::max(P.m, 1));
+    for (int e = 0; e < P.m; ++e) {
+        const pase_edge& x = P.edges[e];
+        const bool later_is_src = P.rank[x.src] > P.rank[x.dst];
+        ed[e].row = later_is_src ? x.src : x.dst;
+        ed[e].col = later_is_src ? x.dst : x.src;
+        ed[e].kcol = P.K[ed[e].col];
+        ed[e].pad = 0;
+        ed[e].off = P.woff[e];
+    }
+    CUDA_TRY(cudaMallocAsync((void**)ed_dev, sizeof(pase::EvalEdge) * ed.size(), ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(*ed_dev, ed.data(), sizeof(pase::EvalEdge) * ed.size(), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));         // ed (pageable) consumed
+    return PASE_OK;
+}
+}  // namespace
+
+pase_status pase_evaluate(pase_ctx* ctx, const int32_t* config_index, int64_t n_strategies, double* cost_out) {
+    if (!ctx || n_strategies < 0 || (n_strategies > 0 && (!config_index || !cost_out))) return PASE_ERR_INVALID;
+    if (ctx->dev < 0) { ctx->err = "host-only planning context: no device evaluation"; return PASE_ERR_STATE; }
+    if (ctx->launched) { ctx->err = "pase_evaluate during a launched solve"; return PASE_ERR_STATE; }
+    const Plan& P = ctx->P;
+    for (int64_t s = 0; s < n_strategies; ++s)
+        for (int v = 0; v < P.n; ++v) {
+            const int32_t c = config_index[s * P.n + v];
+            if (c < 0 || c >= P.K[v]) {
+                ctx->err = "pase_evaluate: strategy " + std::to_string(s) + ", node " + std::to_string(v) +
+                           ": config index " + std::to_string(c) + " outside [0, " + std::to_string(P.K[v]) + ")";
+                return PASE_ERR_INVALID;
+            }
+        }
+    pase::EvalEdge* ed = nullptr;
+    pase_status st = eq1_prepare(ctx, &ed);
+    if (st) return st;
+    if (n_strategies > 0) {
+        int32_t* d_s = nullptr;
+        double* d_c = nullptr;
+        const size_t sb = sizeof(int32_t) * (size_t)n_strategies * P.n, cb = sizeof(double) * (size_t)n_strategies;
+        CUDA_TRY(cudaMallocAsync((void**)&d_s, sb, ctx->stream));
+        CUDA_TRY(cudaMallocAsync((void**)&d_c, cb, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(d_s, config_index, sb, cudaMemcpyHostToDevice, ctx->stream));
+        pase::launch_eval(P.n, P.m, ctx->d_loff, ctx->d_L, ed, ctx->d_W, d_s, n_strategies, d_c, ctx->stream);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(cost_out, d_c, cb, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaFreeAsync(d_s, ctx->stream));
+        CUDA_TRY(cudaFreeAsync(d_c, ctx->stream));
+    }
+    CUDA_TRY(cudaFreeAsync(ed, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return PASE_OK;
+}
+
+pase_status pase_brute_force(pase_ctx* ctx, uint64_t max_strategies, int32_t* config_index_out,
+                             double* total_cost_out, uint64_t* n_strategies_out) {
+    if (!ctx) return PASE_ERR_INVALID;
+    if (ctx->dev < 0) { ctx->err = "host-only planning context: no device search"; return PASE_ERR_STATE; }
+    if (ctx->launched) { ctx->err = "pase_brute_force during a launched solve"; return PASE_ERR_STATE; }
+    const Plan& P = ctx->P;
+    const uint64_t cap = max_strategies ? max_strategies : (1ull << 40);
+    uint64_t total = 1;
+    for (int v = 0; v < P.n; ++v) {
+        if (total > cap / (uint64_t)P.K[v]) {
+            ctx->err = "brute force: prod_v K_v exceeds the limit of " + std::to_string(cap) + " strategies";
+            return PASE_ERR_RESOURCE;
+        }
+        total *= (uint64_t)P.K[v];
+    }
+    if (n_strategies_out) *n_strategies_out = total;
+    int maxsm = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->dev));
+    if (pase::brute_smem_bytes(P.n, P.m) > (size_t)maxsm) {
+        ctx->err = "brute force: graph too large for the shared-memory odometer (" + std::to_string(P.n) + " nodes)";
+        return PASE_ERR_RESOURCE;
+    }
+    pase::EvalEdge* ed = nullptr;
+    pase_status st = eq1_prepare(ctx, &ed);
+    if (st) return st;
+    int sms = 148;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev));
+    const uint64_t want = (total + pase::kBruteThreads - 1) / pase::kBruteThreads;
+    const int nblocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)sms * 16, want));
+    double* d_b = nullptr;
+    uint64_t* d_i = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&d_b, sizeof(double) * (nblocks + 1), ctx->stream));
+    CUDA_TRY(cudaMallocAsync((void**)&d_i, sizeof(uint64_t) * (nblocks + 1), ctx->stream));
+    if (pase::launch_brute(P.n, P.m, ctx->d_K, ctx->d_loff, ctx->d_L, ed, ctx->d_W, total, nblocks, d_b, d_i,
+                           d_b + nblocks, d_i + nblocks, ctx->stream)) {
+        ctx->err = "brute force: cannot reserve shared memory";
+        return PASE_ERR_CUDA;
+    }
+    CUDA_TRY(cudaGetLastError());
+    double best = 0.0;
+    uint64_t bi = 0;
+    CUDA_TRY(cudaMemcpyAsync(&best, d_b + nblocks, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(&bi, d_i + nblocks, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaFreeAsync(d_b, ctx->stream));
+    CUDA_TRY(cudaFreeAsync(d_i, ctx->stream));
+    CUDA_TRY(cudaFreeAsync(ed, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (bi >= total) { ctx->err = "internal: brute force found no strategy"; return PASE_ERR_STATE; }
+    for (int v = 0; v < P.n; ++v) {                          // mixed radix, node 0 fastest
+        if (config_index_out) config_index_out[v] = (int32_t)(bi % (uint64_t)P.K[v]);
+        bi /= (uint64_t)P.K[v];
+    }
+    if (total_cost_out) *total_cost_out = best;
     return PASE_OK;
 }
 

@@ -156,6 +156,13 @@ struct BtDesc {               // back-substitution record of one rank, in back-l
     int32_t radix[kMaxDep];
 };
 
+struct EvalEdge {             // Eq. 1 kernels (eval.cu): W_e element = W[off + c_row * kcol + c_col]
+    int32_t row, col;        // node ids: later- / earlier-ranked endpoint (the DP layout of W_e)
+    int32_t kcol, pad;       // K of the column node
+    int64_t off;             // W_e offset (doubles)
+};
+constexpr int kBruteThreads = 128;
+
 // kernels.cu entry points (host-side launchers)
 void launch_cost_tables(const pase_node* nodes_dev, const int32_t* K_dev, const int64_t* cfg_off_dev,
                         const int32_t* cfg_dev, const int64_t* loff_dev, int n,
@@ -170,5 +177,13 @@ void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev,
 int persistent_blocks_per_sm();
 void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,
                       const double* root_T, int32_t* choice_dev, double* total_dev, void* stream);
+
+// eval.cu (row f2): Eq. 1 for given strategies; exhaustive minimum over all strategies
+void launch_eval(int n, int m, const int64_t* loff_dev, const double* L_dev, const EvalEdge* ed_dev,
+                 const double* W_dev, const int32_t* strat_dev, int64_t ns, double* out_dev, void* stream);
+size_t brute_smem_bytes(int n, int m);
+int launch_brute(int n, int m, const int32_t* K_dev, const int64_t* loff_dev, const double* L_dev,
+                 const EvalEdge* ed_dev, const double* W_dev, uint64_t total, int nblocks,
+                 double* blk_b, uint64_t* blk_i, double* out_b, uint64_t* out_i, void* stream);
 
 }  // namespace pase

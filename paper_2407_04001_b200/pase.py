@@ -89,7 +89,8 @@ class pase_stats(C.Structure):
 EXPORTS = ["pase_create", "pase_solve", "pase_get_stats", "pase_last_error", "pase_destroy",
            "pase_get_configs", "pase_get_order", "pase_get_cost_tables", "pase_get_dp_table",
            "pase_table_entries", "pase_set_cost_tables", "pase_set_profiling", "pase_get_trace",
-           "pase_launch", "pase_finish", "pase_export_handle", "pase_connect", "pase_get_schedule"]
+           "pase_launch", "pase_finish", "pase_export_handle", "pase_connect", "pase_get_schedule",
+           "pase_evaluate", "pase_brute_force"]
 
 _lib = None
 
@@ -133,7 +134,9 @@ def load(path: str = SO):
     L.pase_connect.argtypes = [ctx_p, C.c_void_p]
     L.pase_get_schedule.argtypes = [ctx_p, P(C.c_int32), P(C.c_int64), P(C.c_int32)]
     L.pase_get_schedule.restype = C.c_int64
-    for f in ("pase_create", "pase_solve", "pase_get_stats", "pase_get_configs", "pase_get_order",
+    L.pase_evaluate.argtypes = [ctx_p, P(C.c_int32), C.c_int64, P(C.c_double)]
+    L.pase_brute_force.argtypes = [ctx_p, C.c_uint64, P(C.c_int32), P(C.c_double), P(C.c_uint64)]
+    for f in ("pase_evaluate", "pase_brute_force", "pase_create", "pase_solve", "pase_get_stats", "pase_get_configs", "pase_get_order",
               "pase_get_cost_tables", "pase_get_dp_table", "pase_set_cost_tables", "pase_set_profiling",
               "pase_launch", "pase_finish", "pase_export_handle", "pase_connect"):
         getattr(L, f).restype = C.c_int
@@ -268,6 +271,25 @@ class Context:
         self._chk(self._L.pase_solve(self._h, _ptr(cfg, C.c_int32), _ptr(idx, C.c_int32), C.byref(tot)))
         tuples = [tuple(int(c) for c in cfg[v, :len(self.graph["nodes"][v]["dims"])]) for v in range(self.n)]
         return {"cost": tot.value, "config_index": idx, "configs": tuples}
+
+    # ---- row f2: Eq. 1 on the GPU
+    def evaluate(self, config_index) -> np.ndarray:
+        """pase_evaluate: Eq. 1 cost of each strategy (rows of config indices, one per node)."""
+        a = np.ascontiguousarray(np.atleast_2d(np.asarray(config_index, dtype=np.int32)))
+        if a.shape[1] != self.n:
+            raise ValueError(f"strategies must have {self.n} entries, got {a.shape[1]}")
+        out = np.zeros(a.shape[0], np.float64)
+        self._chk(self._L.pase_evaluate(self._h, _ptr(a, C.c_int32), a.shape[0], _ptr(out, C.c_double)))
+        return out
+
+    def brute_force(self, max_strategies: int = 0) -> Dict[str, object]:
+        """pase_brute_force: min of Eq. 1 over all prod K_v strategies (lowest index wins ties)."""
+        idx = np.zeros(self.n, np.int32)
+        tot = C.c_double()
+        ns = C.c_uint64()
+        self._chk(self._L.pase_brute_force(self._h, max_strategies, _ptr(idx, C.c_int32), C.byref(tot),
+                                           C.byref(ns)))
+        return {"cost": tot.value, "config_index": idx, "n_strategies": ns.value}
 
     def launch(self) -> None:
         """pase_launch: enqueue one solve (a multi-GPU group launches every rank first)."""
