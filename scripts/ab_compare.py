@@ -16,7 +16,7 @@ key, p, policy, _ = WORKLOADS[wl]
 g = zoo.bench_graph(key)[0]
 res = {}
 for k, envs in enumerate(sys.argv[2:4]):
-    for e in ("PASE_NO_2D", "PASE_C_PER_LANE", "PASE_WIDE_WAVES"):
+    for e in ("PASE_NO_2D", "PASE_C_PER_LANE", "PASE_WIDE_WAVES", "PASE_SPREAD", "PASE_SPREAD_TASKS", "PASE_WAVE_TAIL"):
         os.environ.pop(e, None)
     for kv in envs.split():
         a, b = kv.split("=")
