@@ -210,6 +210,24 @@ pase_status pase_evaluate(pase_ctx* ctx, const int32_t* config_index, int64_t n_
 pase_status pase_brute_force(pase_ctx* ctx, uint64_t max_strategies, int32_t* config_index_out,
                              double* total_cost_out, uint64_t* n_strategies_out);
 
+/* ---- device assignment (assign.cpp) --------------------------------------
+ * A strategy fixes how each vertex is split, not which device runs which part; PaSE places the
+ * parts with "a simple greedy assignment that maximizes data locality".  Reading U
+ * (DESIGN §2): shard s of v = the digits of s in the radix of v's split tuple (dim 0 most
+ * significant); vertices in node-id order, shards in index order, each on the free device with
+ * the largest summed overlap (elements) between what consumer shards need of a producer's
+ * output and what the producer shard on that device holds, over edges to placed neighbours;
+ * ties -> lowest device id.  Host-side integer work; also valid on host-only contexts.
+ *   config_index: int32[n_nodes], index of phi(v) in C(v) (e.g. pase_solve's output).
+ *   device_out:   int32[n_nodes * p] (may be NULL): row v = device of each shard, -1 past the
+ *                 shard count prod c(v).
+ *   tx_out:       double[n_edges] (may be NULL): realized t_x bytes of each edge under the
+ *                 assignment, 2 elem max_d (|needed on d| - |needed on d ∩ held on d|)
+ *                 (P:271-276); never below the cost model's aligned t_x (reading K).
+ * PASE_ERR_INVALID names the first config index outside [0, K_v). */
+pase_status pase_assign_devices(const pase_ctx* ctx, const int32_t* config_index, int32_t* device_out,
+                                double* tx_out);
+
 /* ---- split solve (a multi-GPU group launches every rank before waiting on any) ---------- */
 pase_status pase_launch(pase_ctx* ctx);       /* enqueue one solve on the context's stream */
 pase_status pase_finish(pase_ctx* ctx, int32_t* configs_out, int32_t* config_index_out,

@@ -741,3 +741,128 @@ double or_sum_h(int n, int m, const int64_t* edges, const int32_t* K, const doub
     free(woff); free(loff); free(rank);
     return acc;
 }
+
+/* ---------------------------------------------------------------- f3: device assignment */
+/* Greedy device assignment ("a simple greedy assignment that maximizes data
+ * locality, i.e. maximizes |A(v,d,phi) ∩ A(u,d,phi)|"), DESIGN reading U:
+ *   shard s of v under config c = digits of s in the radix c, dim 0 most significant;
+ *   vertices in node-id order, shards in index order; each shard takes the free device with
+ *   the largest sum, over the edges to already-assigned neighbours, of the overlap (elements)
+ *   between what the consumer shard on that device needs of the producer's output tensor and
+ *   what the producer shard on that device holds; ties -> lowest device id.
+ * Realized t_x of an edge = 2 elem max over devices d holding a consumer shard of
+ * (|needed on d| - |needed on d ∩ held on d|), bytes. */
+static void digits_of(const int32_t* c, int d, int s, int* out)
+{
+    for (int k = d - 1; k >= 0; --k) { out[k] = s % c[k]; s /= c[k]; }
+}
+
+/* producer u (config cu, shard digits iu): held interval of output axis a */
+static void held_interval(const int64_t* ru, const int32_t* cu, const int* iu, int a,
+                          int64_t* lo, int64_t* hi)
+{
+    int k = nd_out(ru, a);
+    int64_t h = nd_size(ru, k) / cu[k];
+    *lo = (int64_t)iu[k] * h;
+    *hi = *lo + h;
+}
+
+/* consumer v (config cv, shard digits jv) of edge e: needed interval of u's output axis a */
+static void need_interval(const int64_t* ru, const int64_t* erec, const int32_t* cv, const int* jv,
+                          int a, int64_t* lo, int64_t* hi)
+{
+    int64_t ext = nd_size(ru, nd_out(ru, a));
+    int64_t mp = erec[2 + a];
+    if (mp < 0) { *lo = 0; *hi = ext; return; }
+    int64_t nd = (ext + cv[mp] - 1) / cv[mp];
+    *lo = (int64_t)jv[mp] * nd;
+    *hi = *lo + nd < ext ? *lo + nd : ext;
+    if (*lo > *hi) *lo = *hi;               /* shard past the tensor's end: needs nothing */
+}
+
+/* |needed by consumer shard jv| and |needed ∩ held by producer shard iu| (elements) */
+static void edge_overlap(const int64_t* ru, const int32_t* cu, const int* iu, const int64_t* erec,
+                         const int32_t* cv, const int* jv, int64_t* need, int64_t* ov)
+{
+    *need = 1;
+    *ov = 1;
+    for (int a = 0; a < nd_nout(ru); ++a) {
+        int64_t nl, nh, hl, hh;
+        need_interval(ru, erec, cv, jv, a, &nl, &nh);
+        *need *= nh - nl;
+        if (!iu) continue;
+        held_interval(ru, cu, iu, a, &hl, &hh);
+        int64_t lo = nl > hl ? nl : hl, hi = nh < hh ? nh : hh;
+        *ov *= hi > lo ? hi - lo : 0;
+    }
+    if (!iu) *ov = 0;
+}
+
+int or_assign(int n, const int64_t* nodes, int m, const int64_t* edges, int p, const int32_t* cfg,
+              int32_t* dev, double* tx)
+{
+    if (or_validate(n, nodes, m, edges)) return 1;
+    int32_t* inv = (int32_t*)malloc(sizeof(int32_t) * (size_t)n * p);   /* shard of v on device d */
+    uint8_t* assigned = (uint8_t*)calloc((size_t)n, 1);
+    for (int64_t k = 0; k < (int64_t)n * p; ++k) { inv[k] = -1; dev[k] = -1; }
+    int iu[OR_MAXD], jv[OR_MAXD];
+    for (int v = 0; v < n; ++v) {
+        const int64_t* rv = NREC(nodes, v);
+        const int32_t* cv = cfg + (size_t)v * OR_MAXD;
+        int shards = 1;
+        for (int k = 0; k < nd_dims(rv); ++k) shards *= cv[k];
+        if (shards > p) { free(inv); free(assigned); return 1; }
+        for (int s = 0; s < shards; ++s) {
+            int64_t best = -1;
+            int bestd = -1;
+            for (int d = 0; d < p; ++d) {
+                if (inv[(size_t)v * p + d] >= 0) continue;           /* device taken */
+                int64_t score = 0;
+                for (int e = 0; e < m; ++e) {
+                    const int64_t* er = EREC(edges, e);
+                    int a = (int)er[0], b = (int)er[1];
+                    int64_t need, ov;
+                    if (a == v && assigned[b]) {                     /* v produces for b */
+                        int t = inv[(size_t)b * p + d];
+                        if (t < 0) continue;
+                        digits_of(cv, nd_dims(rv), s, iu);
+                        digits_of(cfg + (size_t)b * OR_MAXD, nd_dims(NREC(nodes, b)), t, jv);
+                        edge_overlap(rv, cv, iu, er, cfg + (size_t)b * OR_MAXD, jv, &need, &ov);
+                        score += ov;
+                    } else if (b == v && assigned[a]) {              /* v consumes from a */
+                        int t = inv[(size_t)a * p + d];
+                        if (t < 0) continue;
+                        digits_of(cfg + (size_t)a * OR_MAXD, nd_dims(NREC(nodes, a)), t, iu);
+                        digits_of(cv, nd_dims(rv), s, jv);
+                        edge_overlap(NREC(nodes, a), cfg + (size_t)a * OR_MAXD, iu, er, cv, jv, &need, &ov);
+                        score += ov;
+                    }
+                }
+                if (score > best) { best = score; bestd = d; }
+            }
+            dev[(size_t)v * p + s] = bestd;
+            inv[(size_t)v * p + bestd] = s;
+        }
+        assigned[v] = 1;
+    }
+    for (int e = 0; e < m; ++e) {
+        const int64_t* er = EREC(edges, e);
+        int a = (int)er[0], b = (int)er[1];
+        const int64_t* ra = NREC(nodes, a);
+        int64_t worst = 0;
+        for (int d = 0; d < p; ++d) {
+            int t = inv[(size_t)b * p + d];
+            if (t < 0) continue;                                     /* d needs nothing */
+            int u = inv[(size_t)a * p + d];
+            digits_of(cfg + (size_t)b * OR_MAXD, nd_dims(NREC(nodes, b)), t, jv);
+            if (u >= 0) digits_of(cfg + (size_t)a * OR_MAXD, nd_dims(ra), u, iu);
+            int64_t need, ov;
+            edge_overlap(ra, cfg + (size_t)a * OR_MAXD, u >= 0 ? iu : NULL, er, cfg + (size_t)b * OR_MAXD, jv,
+                         &need, &ov);
+            if (need - ov > worst) worst = need - ov;
+        }
+        tx[e] = (double)(uint64_t)(2 * nd_elem(ra) * worst);
+    }
+    free(inv); free(assigned);
+    return 0;
+}

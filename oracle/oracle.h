@@ -90,6 +90,12 @@ double or_eval(int n, int m, const int64_t* edges, const int32_t* K, const doubl
 double or_sum_h(int n, int m, const int64_t* edges, const int32_t* K, const double* L,
                 const double* W, const int32_t* sigma, const int32_t* strategy);
 
+/* f3: greedy device assignment (DESIGN reading U).  cfg = the chosen config tuple
+ * of every node (n * OR_MAXD int32).  dev[n * p]: device of shard s of v at dev[v*p + s]
+ * (-1 for s >= prod c(v)); tx[m]: realized t_x bytes of each edge under the assignment. */
+int or_assign(int n, const int64_t* nodes, int m, const int64_t* edges, int p, const int32_t* cfg,
+              int32_t* dev, double* tx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,6 +51,7 @@ def lib():
             "or_dp": [C.c_int, C.c_int, i64p, i32p, f64p, f64p, C.c_int, C.c_int, C.c_int64, i32p, f64p, f64p, i32p],
             "or_dp_bfs_eq2": [C.c_int, C.c_int, i64p, i32p, f64p, f64p, C.c_int64, i32p, f64p],
             "or_brute": [C.c_int, C.c_int, i64p, i32p, f64p, f64p, C.c_int64, i32p, f64p],
+            "or_assign": [C.c_int, i64p, C.c_int, i64p, C.c_int, i32p, i32p, f64p],
         }
         for name, args in sig.items():
             getattr(L, name).argtypes = args
@@ -254,3 +255,18 @@ class Problem:
         s = np.ascontiguousarray(strategy, np.int32)
         sg = np.ascontiguousarray(sigma, np.int32)
         return lib().or_sum_h(*self._args(), _p(sg, C.c_int32), _p(s, C.c_int32))
+
+
+def assign_devices(graph: dict, p: int, tuples) -> Tuple[np.ndarray, np.ndarray]:
+    """f3: greedy device assignment of a strategy given as config tuples per node
+    (P:288-294).  Returns (dev int32[n, p] with -1 padding, realized t_x bytes float64[m])."""
+    N, E = encode(graph)
+    n, m = len(N), len(graph["edges"])
+    cfg = np.ones((n, MAXD), np.int32)
+    for v, t in enumerate(tuples):
+        cfg[v, :len(t)] = t
+    dev = np.zeros((n, p), np.int32)
+    tx = np.zeros(max(m, 1), np.float64)
+    _chk(lib().or_assign(n, _p(N, C.c_int64), m, _p(E, C.c_int64), p, _p(cfg, C.c_int32), _p(dev, C.c_int32),
+                         _p(tx, C.c_double)), "or_assign")
+    return dev, tx[:m]

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libpase.so")
-SOURCES = ["host.cpp", "schedule.cpp", "kernels.cu", "eval.cu", "capi.cu"]
+SOURCES = ["host.cpp", "schedule.cpp", "assign.cpp", "kernels.cu", "eval.cu", "capi.cu"]
 HEADERS = ["pase_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

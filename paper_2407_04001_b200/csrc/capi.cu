@@ -1198,4 +1198,12 @@ pase_status pase_brute_force(pase_ctx* ctx, uint64_t max_strategies, int32_t* co
     return PASE_OK;
 }
 
+// ---- row f3: device assignment (assign.cpp) ------------------------------------------------
+pase_status pase_assign_devices(const pase_ctx* ctx_c, const int32_t* config_index, int32_t* device_out,
+                                double* tx_out) {
+    pase_ctx* ctx = const_cast<pase_ctx*>(ctx_c);
+    if (!ctx || !config_index) return PASE_ERR_INVALID;
+    return pase::assign_devices(ctx->P, config_index, device_out, tx_out, ctx->err);
+}
+
 }  // extern "C"

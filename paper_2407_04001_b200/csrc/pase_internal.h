@@ -178,6 +178,10 @@ int persistent_blocks_per_sm();
 void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,
                       const double* root_T, int32_t* choice_dev, double* total_dev, void* stream);
 
+// assign.cpp (row f3): greedy device assignment of a strategy (DESIGN reading U)
+pase_status assign_devices(const Plan& P, const int32_t* config_index, int32_t* device_out, double* tx_out,
+                           std::string& err);
+
 // eval.cu (row f2): Eq. 1 for given strategies; exhaustive minimum over all strategies
 void launch_eval(int n, int m, const int64_t* loff_dev, const double* L_dev, const EvalEdge* ed_dev,
                  const double* W_dev, const int32_t* strat_dev, int64_t ns, double* out_dev, void* stream);

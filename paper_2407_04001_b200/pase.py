@@ -90,7 +90,7 @@ EXPORTS = ["pase_create", "pase_solve", "pase_get_stats", "pase_last_error", "pa
            "pase_get_configs", "pase_get_order", "pase_get_cost_tables", "pase_get_dp_table",
            "pase_table_entries", "pase_set_cost_tables", "pase_set_profiling", "pase_get_trace",
            "pase_launch", "pase_finish", "pase_export_handle", "pase_connect", "pase_get_schedule",
-           "pase_evaluate", "pase_brute_force"]
+           "pase_evaluate", "pase_brute_force", "pase_assign_devices"]
 
 _lib = None
 
@@ -136,7 +136,8 @@ def load(path: str = SO):
     L.pase_get_schedule.restype = C.c_int64
     L.pase_evaluate.argtypes = [ctx_p, P(C.c_int32), C.c_int64, P(C.c_double)]
     L.pase_brute_force.argtypes = [ctx_p, C.c_uint64, P(C.c_int32), P(C.c_double), P(C.c_uint64)]
-    for f in ("pase_evaluate", "pase_brute_force", "pase_create", "pase_solve", "pase_get_stats", "pase_get_configs", "pase_get_order",
+    L.pase_assign_devices.argtypes = [ctx_p, P(C.c_int32), P(C.c_int32), P(C.c_double)]
+    for f in ("pase_assign_devices", "pase_evaluate", "pase_brute_force", "pase_create", "pase_solve", "pase_get_stats", "pase_get_configs", "pase_get_order",
               "pase_get_cost_tables", "pase_get_dp_table", "pase_set_cost_tables", "pase_set_profiling",
               "pase_launch", "pase_finish", "pase_export_handle", "pase_connect"):
         getattr(L, f).restype = C.c_int
@@ -229,7 +230,7 @@ class Context:
         bandwidth = bandwidth if bandwidth is not None else mach_d.get("bandwidth", 1e10)
         pol = POLICIES[policy] if isinstance(policy, str) else int(policy)
         self.graph = graph
-        self.n, self.m = len(graph["nodes"]), len(graph["edges"])
+        self.n, self.m, self.p = len(graph["nodes"]), len(graph["edges"]), int(p)
         g, self._keep = marshal_graph(graph)
         order = ORDERINGS[ordering] if isinstance(ordering, str) else int(ordering)
         self._mach = make_machine(flops, bandwidth, pol, device, stream, rank, world, virtual_ranks,
@@ -290,6 +291,17 @@ class Context:
         self._chk(self._L.pase_brute_force(self._h, max_strategies, _ptr(idx, C.c_int32), C.byref(tot),
                                            C.byref(ns)))
         return {"cost": tot.value, "config_index": idx, "n_strategies": ns.value}
+
+    # ---- row f3: device assignment
+    def assign_devices(self, config_index):
+        """pase_assign_devices: greedy placement of each vertex's shards on the p devices
+        (P:288-294).  Returns (device int32[n, p] with -1 padding, realized t_x bytes[m])."""
+        idx = np.ascontiguousarray(np.asarray(config_index, dtype=np.int32))
+        dev = np.zeros((self.n, self.p), np.int32)
+        tx = np.zeros(max(self.m, 1), np.float64)
+        self._chk(self._L.pase_assign_devices(self._h, _ptr(idx, C.c_int32), _ptr(dev, C.c_int32),
+                                              _ptr(tx, C.c_double)))
+        return dev, tx[:self.m]
 
     def launch(self) -> None:
         """pase_launch: enqueue one solve (a multi-GPU group launches every rank first)."""
