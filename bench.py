@@ -166,11 +166,20 @@ def main():
 
     import torch
     from paper_2407_04001_b200 import pase, zoo
-    torch.cuda.set_device(local_rank)
+    # PASE_BENCH_SHARE_GPU=1 (functional test of the multi-process group on a 1-GPU box): every
+    # rank uses cuda:0 with 1/world of its SMs (virtual_ranks) and gloo for the host plumbing;
+    # the DP path is the same cross-process CUDA-IPC one, but kernels of different processes
+    # time-slice on one GPU, so the timing is meaningless
+    share = os.environ.get("PASE_BENCH_SHARE_GPU") == "1" and world > 1
+    device = 0 if share else local_rank
+    torch.cuda.set_device(device)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     key, p, policy, desc = WORKLOADS[args.workload]
     graph = zoo.bench_graph(key)[0]
     stream = torch.cuda.Stream()
@@ -179,8 +188,8 @@ def main():
     def make_ctx():
         # one rank per GPU; a group exchanges CUDA-IPC handles over torch.distributed, then
         # the DP kernel moves partitions over NVLink itself (pase_connect)
-        c = pase.Context(graph, p, policy=policy, device=local_rank, stream=stream.cuda_stream,
-                         rank=rank, world=world)
+        c = pase.Context(graph, p, policy=policy, device=device, stream=stream.cuda_stream,
+                         rank=rank, world=world, virtual_ranks=share)
         if world > 1:
             hs = [None] * world
             dist.all_gather_object(hs, c.export_handle())
@@ -200,7 +209,7 @@ def main():
         torch.cuda.synchronize()
 
     step_ms, dp_ms, tab_ms = [], [], []
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(device) as clk:
         barrier()
         for _ in range(args.steps):
             with torch.cuda.stream(stream):
@@ -218,7 +227,7 @@ def main():
         time.sleep(0.25)
     tot_ms = sum(step_ms)
     if dist is not None:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([tot_ms], dtype=torch.float64, device="cpu" if share else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     value = cand * args.steps / (tot_ms / 1e3)
@@ -241,7 +250,7 @@ def main():
             e2e_ms.append(e0.elapsed_time(e1))
     e2e_tot = sum(e2e_ms)
     if dist is not None:
-        t = torch.tensor([e2e_tot], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_tot], dtype=torch.float64, device="cpu" if share else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_tot = float(t.item())
     e2e_value = cand * len(e2e_ms) / (e2e_tot / 1e3)

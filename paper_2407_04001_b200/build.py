@@ -34,20 +34,27 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = SO, defines=()) -> str:
+    """Build libpase.so; `out` / `defines` build an A/B variant next to it (tuning only)."""
+    if not force and out == SO and not _stale():
         return SO
-    cmd = [NVCC, *NVCC_FLAGS, "-shared", "-o", SO + ".tmp", *[os.path.join(CSRC, f) for f in SOURCES], "-ldl"]
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-o", out + ".tmp",
+           *[os.path.join(CSRC, f) for f in SOURCES], "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc build of libpase.so failed")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(SO)
+    if "--variant" in sys.argv:        # python build.py --variant NAME DEF=VAL ...
+        k = sys.argv.index("--variant")
+        name, defs = sys.argv[k + 1], sys.argv[k + 2:]
+        print(build(force=True, out=os.path.join(HERE, f"libpase_{name}.so"), defines=defs))
+    else:
+        build(force="--force" in sys.argv, verbose=True)
+        print(SO)

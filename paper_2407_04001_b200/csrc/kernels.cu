@@ -12,6 +12,11 @@
 
 #include "pase_internal.h"
 
+#ifndef PASE_CUNROLL
+#define PASE_CUNROLL 2   // C iterations in flight per lane in the 1-D tile loop
+#endif
+constexpr int kCUnroll = PASE_CUNROLL;
+
 namespace pase {
 
 // =====================================================================================
@@ -253,7 +258,7 @@ __device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td
         const int Kv = nb > 0 ? vd.K : 0;
         const int jmax = nb > 0 ? nb - 1 : 0;
         const int cstep = G << wlog;
-#pragma unroll 2
+#pragma unroll kCUnroll
         for (int C = lane + (wsub << LG); C < Kv; C += cstep) {   // unrolled: 2 C in flight
             double pre = ld(pp[0] + C);                     // L[C] (term 0 is never in the suffix)
 #pragma unroll

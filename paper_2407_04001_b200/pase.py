@@ -102,10 +102,12 @@ class PaseError(RuntimeError):
 
 
 def load(path: str = SO):
-    """Load libpase.so (no fallback: a missing library is an error)."""
+    """Load libpase.so (no fallback: a missing library is an error).  PASE_LIB names an A/B
+    build variant of it (tuning only)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("PASE_LIB", path)
     if not os.path.exists(path):
         raise ImportError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
     L = C.CDLL(path)
