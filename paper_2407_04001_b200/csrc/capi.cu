@@ -189,12 +189,29 @@ bool no_2d() {
 // multi-GPU partition coordinate) whose first term is latest; use the 2-D tile when its
 // segment structure fits the kernel and it cuts the loads per candidate by >= 20 % on a
 // vertex whose 1-D form is load-heavy.
+// single-suffix 2-D tile only for vertices with at least this many candidates
+const int64_t kMin2S = std::getenv("PASE_MIN_2S") ? std::atoll(std::getenv("PASE_MIN_2S")) : (int64_t(1) << 24);
+
+void set_tile2(VertexDesc& d, int q2, int f2) {
+    d.q2 = q2;
+    d.rq2 = d.radix[q2];
+    d.t2star = f2;
+    d.ostride_q2 = 1;
+    for (int q = 0; q < q2; ++q) d.ostride_q2 *= d.radix[q];
+    d.ntile2 = (d.rq2 + pase::kTile2 - 1) / pase::kTile2;
+    d.ntile = ((d.rq + pase::kTile1 - 1) / pase::kTile1) * d.ntile2;
+    d.ncombo = d.nout / ((int64_t)d.rq * d.rq2);
+    d.nitems = d.ncombo * d.ntile;
+}
+
 void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
     (void)ctx;
     if (d.qstar < 0 || d.m < 2 || d.rq < 2) return;
-    // measured (profiles/r01_ab_*.txt): the 1-D tile is faster except with >= 2 suffix
-    // terms, where its per-candidate loads dominate
-    if (d.nterms - d.tstar < 2) return;
+    // measured (profiles/r01_ab_*.txt): the general 2-D tile is faster than the 1-D one only
+    // with >= 2 suffix terms; one suffix term takes the single-suffix 2-D form when the terms
+    // have its structure (below)
+    static const bool single = !(std::getenv("PASE_2S") && std::getenv("PASE_2S")[0] == '0');
+    if (d.nterms - d.tstar < 2 && !single) return;
     int q2 = -1, f2 = -1;
     for (int q = 0; q < d.m; ++q) {
         if (q == d.qstar || (d.part && q == top) || d.radix[q] < 2) continue;
@@ -205,6 +222,18 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
     }
     if (q2 < 0 || f2 < 1) return;
     const int nP0 = f2, nP1 = d.tstar - f2, NS = d.nterms - d.tstar;
+    if (NS == 1) {
+        // single-suffix form: nP0 terms on neither tiled coordinate, one term on q2 only (it
+        // is the first term on q2 and precedes tstar, so not on qstar), the suffix on qstar only
+        // (small vertices keep the 1-D tile: twice the items, so twice the parallelism, which
+        // is what a latency-bound vertex needs -- measured on InceptionV3)
+        if (nP0 > 3 || nP1 != 1 || tv[d.tstar].stride[q2] != 0 || d.nout * d.K < kMin2S) return;
+        for (int t = 0; t < d.nterms; ++t)
+            if (tv[t].stride[q2] >= (int64_t(1) << 31) / 16) return;
+        set_tile2(d, q2, f2);
+        d.shape = pase::kShape2S + (nP0 - 1) * 4 + (d.glog - 2);
+        return;
+    }
     if (nP0 > pase::kMaxP0 || nP1 > pase::kMaxP1 || NS < 1 || NS > 2) return;
     if (NS == 2 && (tv[d.tstar].stride[q2] != 0 || tv[d.tstar + 1].stride[q2] != 0)) return;
     for (int t = 0; t < d.nterms; ++t)
@@ -215,15 +244,7 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
     const double per2 = l2 / (pase::kTile1 * pase::kTile2);
     const double per1 = (double)(d.tstar + pase::kTile * NS) / pase::kTile;
     if (per2 > 0.8 * per1) return;
-    d.q2 = q2;
-    d.rq2 = d.radix[q2];
-    d.t2star = f2;
-    d.ostride_q2 = 1;
-    for (int q = 0; q < q2; ++q) d.ostride_q2 *= d.radix[q];
-    d.ntile2 = (d.rq2 + pase::kTile2 - 1) / pase::kTile2;
-    d.ntile = ((d.rq + pase::kTile1 - 1) / pase::kTile1) * d.ntile2;
-    d.ncombo = d.nout / ((int64_t)d.rq * d.rq2);
-    d.nitems = d.ncombo * d.ntile;
+    set_tile2(d, q2, f2);
     d.shape = pase::kShape2D + (NS - 1) * 4 + (d.glog - 2);
 }
 

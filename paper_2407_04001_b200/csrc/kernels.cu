@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "pase_internal.h"
 
@@ -178,6 +179,12 @@ struct Log2<1> { static constexpr int value = 0; };
 __device__ __forceinline__ double ld(const double* p) {
     double v;
     asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+template <int OFF>                       // element offset folded into the instruction
+__device__ __forceinline__ double ld_at(const double* p) {
+    double v;
+    asm volatile("ld.global.f64 %0, [%1+%2];" : "=d"(v) : "l"(p), "n"(OFF * 8));
     return v;
 }
 __device__ __forceinline__ void st_f64(double* p, double v) {
@@ -498,6 +505,150 @@ __device__ __noinline__ void tile2_items(const VertexDesc& vd, const TermDesc* t
     }
 }
 
+// 2-D register tile, single-suffix form (shape >= kShape2S): the structure of
+// the big vertices of the zoo -- NP0 terms that depend on neither tiled coordinate, exactly one
+// term depending on q2 (not q1), then exactly one term depending on q1 (not q2):
+//   cost(j1, j2) = ((P0 terms) + T_p1[q2 = j2]) + T_s[q1 = j1]      (canonical order kept)
+// Per C a lane loads NP0 + 4 + 4 values for 16 candidates (the 1-D tile: NP + 8 for 8), and
+// every address is a per-item pointer + C (no per-iteration stride arithmetic).
+template <int NP0, int G>
+__device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* td, int64_t first,
+                                          int64_t stride, int64_t end) {
+    constexpr int V1 = kTile1, V2 = kTile2, V = V1 * V2;
+    constexpr int LG = Log2<G>::value, LV = Log2<V>::value;
+    constexpr int S = LG < LV ? LG : LV;
+    constexpr int H = V >> S;
+    const int lane = threadIdx.x & (G - 1);
+    const int sub = (threadIdx.x & 31) / G;
+    const int q1 = vd.qstar, q2 = vd.q2;
+    const int64_t sb = td[NP0].stride[q2], ss = td[NP0 + 1].stride[q1];
+    for (int64_t base = first; base < end; base += stride) {
+        const int64_t item = base + sub;
+        const bool valid = item < end;
+        const uint32_t it = valid ? (uint32_t)item : 0u;
+        const uint32_t nc = (uint32_t)vd.ncombo;
+        uint32_t rem = it % nc;
+        const uint32_t tidx = it / nc;
+        const int x2 = (int)(tidx % (uint32_t)vd.ntile2) * V2;
+        const int x1 = (int)(tidx / (uint32_t)vd.ntile2) * V1;
+        const int nb1 = valid ? min(V1, vd.rq - x1) : 0;
+        const int nb2 = valid ? min(V2, vd.rq2 - x2) : 0;
+        const double* pa[NP0];
+#pragma unroll
+        for (int t = 0; t < NP0; ++t) pa[t] = td[t].base;
+        const double* pb = td[NP0].base + (int64_t)x2 * sb;
+        const double* ps = td[NP0 + 1].base + (int64_t)x1 * ss;
+        int64_t obase = 0, ost = 1;
+        for (int c = 0; c < vd.m; ++c) {                    // mixed-radix decode (lowest fastest)
+            const uint32_t r = (uint32_t)vd.radix[c];
+            if (c != q1 && c != q2) {
+                const uint32_t v = rem % r;
+                rem /= r;
+                obase += (int64_t)v * ost;
+#pragma unroll
+                for (int t = 0; t < NP0; ++t) pa[t] += (int64_t)v * td[t].stride[c];
+                pb += (int64_t)v * td[NP0].stride[c];
+                ps += (int64_t)v * td[NP0 + 1].stride[c];
+            }
+            ost *= r;
+        }
+        const int m1 = nb1 > 0 ? nb1 - 1 : 0, m2 = nb2 > 0 ? nb2 - 1 : 0;
+        const double* b[V2];
+        const double* s[V1];
+#pragma unroll
+        for (int j = 0; j < V2; ++j) b[j] = pb + (int64_t)min(j, m2) * sb;   // partial tiles re-read
+#pragma unroll
+        for (int j = 0; j < V1; ++j) s[j] = ps + (int64_t)min(j, m1) * ss;   // a valid row
+        double best[V];
+        int bestC[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) { best[j] = __longlong_as_double(0x7ff0000000000000ll); bestC[j] = 0x7fffffff; }
+        const int Kv = (nb1 > 0 && nb2 > 0) ? vd.K : 0;
+        // pointer induction: every row pointer starts at this lane's C and advances by 2G per
+        // double iteration; the second iteration's loads carry +G as an immediate
+#pragma unroll
+        for (int t = 0; t < NP0; ++t) pa[t] += lane;
+#pragma unroll
+        for (int j = 0; j < V2; ++j) b[j] += lane;
+#pragma unroll
+        for (int j = 0; j < V1; ++j) s[j] += lane;
+        auto step = [&](auto off, int C) {
+            constexpr int O = decltype(off)::value;
+            double pre = ld_at<O>(pa[0]);
+#pragma unroll
+            for (int t = 1; t < NP0; ++t) pre = __dadd_rn(pre, ld_at<O>(pa[t]));
+            double p1[V2], sv[V1];
+#pragma unroll
+            for (int j = 0; j < V2; ++j) p1[j] = ld_at<O>(b[j]);
+#pragma unroll
+            for (int j = 0; j < V1; ++j) sv[j] = ld_at<O>(s[j]);
+#pragma unroll
+            for (int j = 0; j < V2; ++j) p1[j] = __dadd_rn(pre, p1[j]);
+#pragma unroll
+            for (int j1 = 0; j1 < V1; ++j1)
+#pragma unroll
+                for (int j2 = 0; j2 < V2; ++j2) {
+                    const double cost = __dadd_rn(p1[j2], sv[j1]);
+                    const int j = j1 * V2 + j2;
+                    if (cost < best[j]) { best[j] = cost; bestC[j] = C; }   // strict <: lowest C
+                }
+        };
+        int C = lane;
+#pragma unroll 1
+        for (; C + G < Kv; C += 2 * G) {
+            step(std::integral_constant<int, 0>{}, C);
+            step(std::integral_constant<int, G>{}, C + G);
+#pragma unroll
+            for (int t = 0; t < NP0; ++t) pa[t] += 2 * G;
+#pragma unroll
+            for (int j = 0; j < V2; ++j) b[j] += 2 * G;
+#pragma unroll
+            for (int j = 0; j < V1; ++j) s[j] += 2 * G;
+        }
+        if (C < Kv) step(std::integral_constant<int, 0>{}, C);
+        // butterfly reduce-scatter across the G lanes of the group (as tile_items)
+#pragma unroll
+        for (int st = 0; st < S; ++st) {
+            const int o = G >> (st + 1);
+            const int half = V >> (st + 1);
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int k = 0; k < half; ++k) {
+                const double sbv = up ? best[k] : best[k + half];
+                const int sc = up ? bestC[k] : bestC[k + half];
+                double kb = up ? best[k + half] : best[k];
+                int kc = up ? bestC[k + half] : bestC[k];
+                const double rb = __shfl_xor_sync(0xffffffffu, sbv, o);
+                const int rc = __shfl_xor_sync(0xffffffffu, sc, o);
+                combine(kb, kc, rb, rc);
+                best[k] = kb;
+                bestC[k] = kc;
+            }
+        }
+#pragma unroll
+        for (int o = G >> (S + 1); o >= 1; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+                const double rb = __shfl_xor_sync(0xffffffffu, best[k], o);
+                const int rc = __shfl_xor_sync(0xffffffffu, bestC[k], o);
+                combine(best[k], bestC[k], rb, rc);
+            }
+        int jbase = 0;
+#pragma unroll
+        for (int st = 0; st < S; ++st)
+            if (lane & (G >> (st + 1))) jbase += V >> (st + 1);
+        if ((lane & ((G >> S) - 1)) == 0) {
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+                const int j = jbase + k, j1 = j / V2, j2 = j % V2;
+                if (j1 < nb1 && j2 < nb2)
+                    st_out(vd, obase + (int64_t)(x1 + j1) * vd.ostride_q + (int64_t)(x2 + j2) * vd.ostride_q2,
+                           best[k], bestC[k]);
+            }
+        }
+    }
+}
+
 // Generic path (any number of terms, 64-bit strides): one lane group per output phi,
 // offsets recomputed per candidate.  Outputs [first + k*stride + sub, ...) < end.
 __device__ __noinline__ void generic_items(const VertexDesc& vd, const TermDesc* __restrict__ tds, int glog,
@@ -565,6 +716,16 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
         PASE_CASE2(1, 2) PASE_CASE2(1, 3) PASE_CASE2(1, 4) PASE_CASE2(1, 5)
         PASE_CASE2(2, 2) PASE_CASE2(2, 3) PASE_CASE2(2, 4) PASE_CASE2(2, 5)
 #undef PASE_CASE2
+#define PASE_CASE2S(NP0, LGG)                                                                     \
+    case kShape2S + (NP0 - 1) * 4 + (LGG - 2): {                                                  \
+        constexpr int G_ = 1 << LGG, GPW_ = 32 / G_;                                              \
+        tile2s_items<NP0, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1);              \
+        return;                                                                                   \
+    }
+        PASE_CASE2S(1, 2) PASE_CASE2S(1, 3) PASE_CASE2S(1, 4) PASE_CASE2S(1, 5)
+        PASE_CASE2S(2, 2) PASE_CASE2S(2, 3) PASE_CASE2S(2, 4) PASE_CASE2S(2, 5)
+        PASE_CASE2S(3, 2) PASE_CASE2S(3, 3) PASE_CASE2S(3, 4) PASE_CASE2S(3, 5)
+#undef PASE_CASE2S
         default: {
             const int gpw = 32 >> vd.glog;
             generic_items(vd, tds_g, vd.glog, i0 + first_warp * gpw, nwarps * gpw, i1);
