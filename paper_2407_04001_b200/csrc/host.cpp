@@ -4,6 +4,7 @@
 //   a4 elimination tree (children(i) = {j : min-rank D(j) = i}) and layouts.
 // Written independently of oracle/ (bitset d-sets, tree rule instead of dfs).
 #include <algorithm>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <numeric>
@@ -87,25 +88,39 @@ void splits_of(const pase_node& x, int k, int p, std::vector<int>& out) {
 
 // Lexicographic product (dim 0 most significant) filtered by the policy.  Depth-first over
 // the ascending split lists, pruned by the running product; no per-tuple allocation.
+// EXACT_P: `target` = the largest achievable product <= p; only branches that can still reach
+// it exactly are walked (maxrem[k] = product of the largest splits of dims k..).
 struct Enum {
     int nd, p;
+    int64_t target = 0;                        // 0: LE_P (every product <= p)
     int opt[kMaxDims][64], nopt[kMaxDims];
+    int64_t maxrem[kMaxDims + 1];
     int32_t cur[kMaxDims];
     std::vector<int32_t>* rows;
-    std::vector<int64_t> prods;
     void rec(int k, int64_t prod) {
         if (k == nd) {
-            rows->insert(rows->end(), cur, cur + kMaxDims);
-            prods.push_back(prod);
+            if (target == 0 || prod == target) rows->insert(rows->end(), cur, cur + kMaxDims);
             return;
         }
         for (int i = 0; i < nopt[k]; ++i) {
             const int c = opt[k][i];
-            if (prod * c > p) break;          // ascending: larger splits exceed p too
+            const int64_t q = prod * c;
+            if (q > (target ? target : p)) break;       // ascending: larger splits exceed it too
+            if (target && q * maxrem[k + 1] < target) continue;
             cur[k] = c;
-            rec(k + 1, prod * c);
+            rec(k + 1, q);
         }
         cur[k] = 1;
+    }
+    int64_t best(int k, int64_t prod) const {          // largest reachable product <= p
+        if (k == nd) return prod;
+        int64_t b = 0;
+        for (int i = 0; i < nopt[k] && prod * opt[k][i] <= p; ++i) {
+            if (prod * opt[k][i] * maxrem[k + 1] <= b) continue;
+            b = std::max(b, best(k + 1, prod * opt[k][i]));
+            if (b == p) break;
+        }
+        return b;
     }
 };
 
@@ -119,21 +134,14 @@ void enumerate(const pase_node& x, int p, int policy, std::vector<int32_t>& rows
         E.nopt[k] = (int)tmp.size();
         for (int i = 0; i < E.nopt[k]; ++i) E.opt[k][i] = tmp[i];
     }
+    E.maxrem[x.n_dims] = 1;
+    for (int k = x.n_dims - 1; k >= 0; --k)
+        E.maxrem[k] = std::min<int64_t>((int64_t)p, E.maxrem[k + 1] * E.opt[k][E.nopt[k] - 1]);
     for (int k = 0; k < kMaxDims; ++k) E.cur[k] = 1;
     rows.clear();
     E.rows = &rows;
+    if (policy == PASE_CFG_EXACT_P) E.target = E.best(0, 1);   // the tuples of that product only
     E.rec(0, 1);
-    if (policy == PASE_CFG_EXACT_P) {         // keep the tuples of the largest product <= p
-        int64_t target = 0;
-        for (int64_t q : E.prods) target = std::max(target, q);
-        size_t w = 0;
-        for (size_t i = 0; i < E.prods.size(); ++i)
-            if (E.prods[i] == target) {
-                if (w != i) std::copy(rows.begin() + i * kMaxDims, rows.begin() + (i + 1) * kMaxDims, rows.begin() + w * kMaxDims);
-                ++w;
-            }
-        rows.resize(w * kMaxDims);
-    }
 }
 
 // ---------------------------------------------------------------- a3
@@ -226,8 +234,19 @@ pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* mach,
     P.cfg_off.assign(n + 1, 0);
     P.cfg.clear();
     std::vector<int32_t> rows;
+    // C(v) depends only on (n_dims, size[], splittable_mask, p, policy): enumerate each
+    // distinct iteration space once (the zoo's layers repeat per block / time step)
+    std::map<std::vector<int64_t>, std::vector<int32_t>> memo;
     for (int v = 0; v < n; ++v) {
-        enumerate(P.nodes[v], p, P.policy, rows);
+        const pase_node& x = P.nodes[v];
+        std::vector<int64_t> key(x.size, x.size + x.n_dims);
+        key.push_back(x.splittable_mask);
+        auto it = memo.find(key);
+        if (it == memo.end()) {
+            enumerate(x, p, P.policy, rows);
+            it = memo.emplace(std::move(key), rows).first;
+        }
+        rows = it->second;
         int64_t k = (int64_t)rows.size() / kMaxDims;
         if (k < 1 || k > 65535) { err = fmt("node %lld: %lld configurations (supported 1..65535)", v, k); return PASE_ERR_RESOURCE; }
         P.K[v] = (int32_t)k;
