@@ -211,29 +211,46 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
     // with >= 2 suffix terms; one suffix term takes the single-suffix 2-D form when the terms
     // have its structure (below)
     static const bool single = !(std::getenv("PASE_2S") && std::getenv("PASE_2S")[0] == '0');
-    if (d.nterms - d.tstar < 2 && !single) return;
-    int q2 = -1, f2 = -1;
+    const int NSd = d.nterms - d.tstar;
+    // candidate q2 coordinates, best first: latest first term (longest scalar prefix), then
+    // larger radix
+    std::vector<std::pair<int, int>> cand;                 // (first term, q)
     for (int q = 0; q < d.m; ++q) {
         if (q == d.qstar || (d.part && q == top) || d.radix[q] < 2) continue;
         int first = -1;
         for (int t = 0; t < d.nterms && first < 0; ++t)
             if (tv[t].stride[q] != 0) first = t;
-        if (first > f2 || (first == f2 && d.radix[q] > d.radix[q2])) { f2 = first; q2 = q; }
+        cand.push_back({first, q});
     }
+    std::sort(cand.begin(), cand.end(), [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+        return x.first != y.first ? x.first > y.first : d.radix[x.second] > d.radix[y.second];
+    });
+    if (cand.empty()) return;
+    // single-suffix form (tile2s_items): P0 = [0, f2) on neither coordinate; P1 = the first
+    // term on q2 plus NB <= 1 terms not on q2; S = one term on qstar (not q2), optionally one
+    // more not on q2 (on qstar or constant).  Small vertices keep the 1-D tile: twice the
+    // items, i.e. twice the parallelism a latency-bound vertex needs (measured on InceptionV3).
+    if (single && d.nout * d.K >= kMin2S && (d.glog == 2 || d.glog == 3) && NSd <= 2) {
+        for (const auto& cq : cand) {
+            const int q2 = cq.second, f2 = cq.first;
+            const int nb = d.tstar - f2 - 1;
+            if (f2 < 1 || f2 > 3 || nb < 0 || nb > 1 || (NSd == 2 && nb != 0)) continue;
+            bool ok = true;
+            for (int t = f2 + 1; t < d.nterms; ++t) ok = ok && tv[t].stride[q2] == 0;
+            for (int t = 0; t < d.nterms; ++t) ok = ok && tv[t].stride[q2] < (int64_t(1) << 31) / 16;
+            if (!ok) continue;
+            const int form = NSd == 1 ? nb : (tv[d.tstar + 1].stride[d.qstar] != 0 ? 3 : 2);
+            set_tile2(d, q2, f2);
+            d.shape = pase::kShape2S + ((f2 - 1) * 4 + form) * 2 + (d.glog - 2);
+            return;
+        }
+    }
+    // measured (profiles/r01_ab_*.txt): the general 2-D tile is faster than the 1-D one only
+    // with >= 2 suffix terms
+    if (NSd < 2) return;
+    const int q2 = cand[0].second, f2 = cand[0].first;
     if (q2 < 0 || f2 < 1) return;
     const int nP0 = f2, nP1 = d.tstar - f2, NS = d.nterms - d.tstar;
-    if (NS == 1) {
-        // single-suffix form: nP0 terms on neither tiled coordinate, one term on q2 only (it
-        // is the first term on q2 and precedes tstar, so not on qstar), the suffix on qstar only
-        // (small vertices keep the 1-D tile: twice the items, so twice the parallelism, which
-        // is what a latency-bound vertex needs -- measured on InceptionV3)
-        if (nP0 > 3 || nP1 != 1 || tv[d.tstar].stride[q2] != 0 || d.nout * d.K < kMin2S) return;
-        for (int t = 0; t < d.nterms; ++t)
-            if (tv[t].stride[q2] >= (int64_t(1) << 31) / 16) return;
-        set_tile2(d, q2, f2);
-        d.shape = pase::kShape2S + (nP0 - 1) * 4 + (d.glog - 2);
-        return;
-    }
     if (nP0 > pase::kMaxP0 || nP1 > pase::kMaxP1 || NS < 1 || NS > 2) return;
     if (NS == 2 && (tv[d.tstar].stride[q2] != 0 || tv[d.tstar + 1].stride[q2] != 0)) return;
     for (int t = 0; t < d.nterms; ++t)

@@ -506,22 +506,28 @@ __device__ __noinline__ void tile2_items(const VertexDesc& vd, const TermDesc* t
 }
 
 // 2-D register tile, single-suffix form (shape >= kShape2S): the structure of
-// the big vertices of the zoo -- NP0 terms that depend on neither tiled coordinate, exactly one
-// term depending on q2 (not q1), then exactly one term depending on q1 (not q2):
-//   cost(j1, j2) = ((P0 terms) + T_p1[q2 = j2]) + T_s[q1 = j1]      (canonical order kept)
-// Per C a lane loads NP0 + 4 + 4 values for 16 candidates (the 1-D tile: NP + 8 for 8), and
-// every address is a per-item pointer + C (no per-iteration stride arithmetic).
-template <int NP0, int G>
+// the big vertices of the zoo, in canonical term order --
+//   P0: NP0 terms on neither tiled coordinate          (summed once per C: pre)
+//   P1: one term on q2 (not q1), then NB terms on neither   (per q2 value: p1[j2])
+//   S : one term on q1 (not q2), then, FORM-dependent, one more term on q1 (NS2 = 2) or on
+//       neither (NS2 = 1)
+//   cost(j1, j2) = ((((pre + A[j2]) + B..) + S1[j1]) + S2[j1])      (association unchanged)
+// Per C a lane loads NP0 + 4 + NB + 4 (+ 4 or 1) values for 16 candidates (the 1-D tile: NP +
+// 8 NS for 8), every address a per-item row pointer advanced by induction.
+template <int NP0, int NB, int NS2, int G>
 __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* td, int64_t first,
                                           int64_t stride, int64_t end) {
     constexpr int V1 = kTile1, V2 = kTile2, V = V1 * V2;
     constexpr int LG = Log2<G>::value, LV = Log2<V>::value;
     constexpr int S = LG < LV ? LG : LV;
     constexpr int H = V >> S;
+    constexpr int TA = NP0, TS = NP0 + 1 + NB;          // term index of A (P1 head), of S1
+    constexpr int NR2 = NS2 == 2 ? V1 : 1;              // rows of the second suffix term
     const int lane = threadIdx.x & (G - 1);
     const int sub = (threadIdx.x & 31) / G;
     const int q1 = vd.qstar, q2 = vd.q2;
-    const int64_t sb = td[NP0].stride[q2], ss = td[NP0 + 1].stride[q1];
+    const int64_t sb = td[TA].stride[q2], ss = td[TS].stride[q1];
+    const int64_t ss2 = NS2 == 2 ? td[TS + 1].stride[q1] : 0;
     for (int64_t base = first; base < end; base += stride) {
         const int64_t item = base + sub;
         const bool valid = item < end;
@@ -533,11 +539,17 @@ __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* 
         const int x1 = (int)(tidx / (uint32_t)vd.ntile2) * V1;
         const int nb1 = valid ? min(V1, vd.rq - x1) : 0;
         const int nb2 = valid ? min(V2, vd.rq2 - x2) : 0;
+        // row pointers of every term at this item's combination (tiled coordinates at 0)
         const double* pa[NP0];
+        const double* pe[NB > 0 ? NB : 1];
+        const double* pt2;
 #pragma unroll
         for (int t = 0; t < NP0; ++t) pa[t] = td[t].base;
-        const double* pb = td[NP0].base + (int64_t)x2 * sb;
-        const double* ps = td[NP0 + 1].base + (int64_t)x1 * ss;
+#pragma unroll
+        for (int t = 0; t < NB; ++t) pe[t] = td[TA + 1 + t].base;
+        const double* pb = td[TA].base + (int64_t)x2 * sb;
+        const double* ps = td[TS].base + (int64_t)x1 * ss;
+        pt2 = NS2 ? td[TS + 1].base + (int64_t)x1 * ss2 : nullptr;
         int64_t obase = 0, ost = 1;
         for (int c = 0; c < vd.m; ++c) {                    // mixed-radix decode (lowest fastest)
             const uint32_t r = (uint32_t)vd.radix[c];
@@ -547,48 +559,63 @@ __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* 
                 obase += (int64_t)v * ost;
 #pragma unroll
                 for (int t = 0; t < NP0; ++t) pa[t] += (int64_t)v * td[t].stride[c];
-                pb += (int64_t)v * td[NP0].stride[c];
-                ps += (int64_t)v * td[NP0 + 1].stride[c];
+#pragma unroll
+                for (int t = 0; t < NB; ++t) pe[t] += (int64_t)v * td[TA + 1 + t].stride[c];
+                pb += (int64_t)v * td[TA].stride[c];
+                ps += (int64_t)v * td[TS].stride[c];
+                if (NS2) pt2 += (int64_t)v * td[TS + 1].stride[c];
             }
             ost *= r;
         }
         const int m1 = nb1 > 0 ? nb1 - 1 : 0, m2 = nb2 > 0 ? nb2 - 1 : 0;
         const double* b[V2];
         const double* s[V1];
+        const double* s2[NR2];
 #pragma unroll
-        for (int j = 0; j < V2; ++j) b[j] = pb + (int64_t)min(j, m2) * sb;   // partial tiles re-read
+        for (int j = 0; j < V2; ++j) b[j] = pb + (int64_t)min(j, m2) * sb + lane;   // partial tiles
 #pragma unroll
-        for (int j = 0; j < V1; ++j) s[j] = ps + (int64_t)min(j, m1) * ss;   // a valid row
+        for (int j = 0; j < V1; ++j) s[j] = ps + (int64_t)min(j, m1) * ss + lane;   // re-read a
+#pragma unroll
+        for (int j = 0; j < NR2; ++j) s2[j] = NS2 ? pt2 + (int64_t)min(j, m1) * ss2 + lane : nullptr;  // valid row
+#pragma unroll
+        for (int t = 0; t < NP0; ++t) pa[t] += lane;
+#pragma unroll
+        for (int t = 0; t < NB; ++t) pe[t] += lane;
         double best[V];
         int bestC[V];
 #pragma unroll
         for (int j = 0; j < V; ++j) { best[j] = __longlong_as_double(0x7ff0000000000000ll); bestC[j] = 0x7fffffff; }
         const int Kv = (nb1 > 0 && nb2 > 0) ? vd.K : 0;
-        // pointer induction: every row pointer starts at this lane's C and advances by 2G per
-        // double iteration; the second iteration's loads carry +G as an immediate
-#pragma unroll
-        for (int t = 0; t < NP0; ++t) pa[t] += lane;
-#pragma unroll
-        for (int j = 0; j < V2; ++j) b[j] += lane;
-#pragma unroll
-        for (int j = 0; j < V1; ++j) s[j] += lane;
+        // every row pointer starts at this lane's C and advances by 2G per double iteration;
+        // the second iteration's loads carry +G as an immediate
         auto step = [&](auto off, int C) {
             constexpr int O = decltype(off)::value;
             double pre = ld_at<O>(pa[0]);
 #pragma unroll
             for (int t = 1; t < NP0; ++t) pre = __dadd_rn(pre, ld_at<O>(pa[t]));
-            double p1[V2], sv[V1];
+            double p1[V2], sv[V1], tv[NR2], ev[NB > 0 ? NB : 1];
 #pragma unroll
             for (int j = 0; j < V2; ++j) p1[j] = ld_at<O>(b[j]);
 #pragma unroll
-            for (int j = 0; j < V1; ++j) sv[j] = ld_at<O>(s[j]);
+            for (int t = 0; t < NB; ++t) ev[t] = ld_at<O>(pe[t]);
 #pragma unroll
-            for (int j = 0; j < V2; ++j) p1[j] = __dadd_rn(pre, p1[j]);
+            for (int j = 0; j < V1; ++j) sv[j] = ld_at<O>(s[j]);
+            if (NS2) {
+#pragma unroll
+                for (int j = 0; j < NR2; ++j) tv[j] = ld_at<O>(s2[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < V2; ++j) {
+                p1[j] = __dadd_rn(pre, p1[j]);
+#pragma unroll
+                for (int t = 0; t < NB; ++t) p1[j] = __dadd_rn(p1[j], ev[t]);
+            }
 #pragma unroll
             for (int j1 = 0; j1 < V1; ++j1)
 #pragma unroll
                 for (int j2 = 0; j2 < V2; ++j2) {
-                    const double cost = __dadd_rn(p1[j2], sv[j1]);
+                    double cost = __dadd_rn(p1[j2], sv[j1]);
+                    if (NS2) cost = __dadd_rn(cost, tv[NS2 == 2 ? j1 : 0]);
                     const int j = j1 * V2 + j2;
                     if (cost < best[j]) { best[j] = cost; bestC[j] = C; }   // strict <: lowest C
                 }
@@ -601,9 +628,13 @@ __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* 
 #pragma unroll
             for (int t = 0; t < NP0; ++t) pa[t] += 2 * G;
 #pragma unroll
+            for (int t = 0; t < NB; ++t) pe[t] += 2 * G;
+#pragma unroll
             for (int j = 0; j < V2; ++j) b[j] += 2 * G;
 #pragma unroll
             for (int j = 0; j < V1; ++j) s[j] += 2 * G;
+#pragma unroll
+            for (int j = 0; j < NR2; ++j) s2[j] += NS2 ? 2 * G : 0;
         }
         if (C < Kv) step(std::integral_constant<int, 0>{}, C);
         // butterfly reduce-scatter across the G lanes of the group (as tile_items)
@@ -716,15 +747,19 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
         PASE_CASE2(1, 2) PASE_CASE2(1, 3) PASE_CASE2(1, 4) PASE_CASE2(1, 5)
         PASE_CASE2(2, 2) PASE_CASE2(2, 3) PASE_CASE2(2, 4) PASE_CASE2(2, 5)
 #undef PASE_CASE2
-#define PASE_CASE2S(NP0, LGG)                                                                     \
-    case kShape2S + (NP0 - 1) * 4 + (LGG - 2): {                                                  \
+#define PASE_CASE2S(NP0, FORM, NB, NS2, LGG)                                                      \
+    case kShape2S + ((NP0 - 1) * 4 + FORM) * 2 + (LGG - 2): {                                     \
         constexpr int G_ = 1 << LGG, GPW_ = 32 / G_;                                              \
-        tile2s_items<NP0, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1);              \
+        tile2s_items<NP0, NB, NS2, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1);     \
         return;                                                                                   \
     }
-        PASE_CASE2S(1, 2) PASE_CASE2S(1, 3) PASE_CASE2S(1, 4) PASE_CASE2S(1, 5)
-        PASE_CASE2S(2, 2) PASE_CASE2S(2, 3) PASE_CASE2S(2, 4) PASE_CASE2S(2, 5)
-        PASE_CASE2S(3, 2) PASE_CASE2S(3, 3) PASE_CASE2S(3, 4) PASE_CASE2S(3, 5)
+#define PASE_2S_FORMS(NP0)                                                                        \
+        PASE_CASE2S(NP0, 0, 0, 0, 2) PASE_CASE2S(NP0, 0, 0, 0, 3)                                 \
+        PASE_CASE2S(NP0, 1, 1, 0, 2) PASE_CASE2S(NP0, 1, 1, 0, 3)                                 \
+        PASE_CASE2S(NP0, 2, 0, 1, 2) PASE_CASE2S(NP0, 2, 0, 1, 3)                                 \
+        PASE_CASE2S(NP0, 3, 0, 2, 2) PASE_CASE2S(NP0, 3, 0, 2, 3)
+        PASE_2S_FORMS(1) PASE_2S_FORMS(2) PASE_2S_FORMS(3)
+#undef PASE_2S_FORMS
 #undef PASE_CASE2S
         default: {
             const int gpw = 32 >> vd.glog;
