@@ -230,7 +230,14 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
     // term on q2 plus NB <= 1 terms not on q2; S = one term on qstar (not q2), optionally one
     // more not on q2 (on qstar or constant).  Small vertices keep the 1-D tile: twice the
     // items, i.e. twice the parallelism a latency-bound vertex needs (measured on InceptionV3).
-    if (single && d.nout * d.K >= kMin2S && (d.glog == 2 || d.glog == 3) && NSd <= 2) {
+    // Below kMin2S a 4-lane vertex with K >= 128 takes the 2-D form with 8-lane groups: half
+    // the items of the 1-D tile but twice the lanes per item, so the same parallelism, half the
+    // serial C iterations (still >= 16 per lane) and fewer loads per candidate (measured:
+    // Transformer EXACT_P DP 0.571 -> 0.539 ms; with K < 128 the reduction dominates: GNMT
+    // 0.633 -> 0.678 ms, hence the bound).
+    static const bool wide = !(std::getenv("PASE_2S_WIDE") && std::getenv("PASE_2S_WIDE")[0] == '0');
+    const bool big = d.nout * d.K >= kMin2S;
+    if (single && (big || (wide && d.glog == 2 && d.K >= 128)) && (d.glog == 2 || d.glog == 3) && NSd <= 2) {
         for (const auto& cq : cand) {
             const int q2 = cq.second, f2 = cq.first;
             const int nb = d.tstar - f2 - 1;
@@ -240,6 +247,7 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
             for (int t = 0; t < d.nterms; ++t) ok = ok && tv[t].stride[q2] < (int64_t(1) << 31) / 16;
             if (!ok) continue;
             const int form = NSd == 1 ? nb : (tv[d.tstar + 1].stride[d.qstar] != 0 ? 3 : 2);
+            if (!big) d.glog = 3;
             set_tile2(d, q2, f2);
             d.shape = pase::kShape2S + ((f2 - 1) * 4 + form) * 2 + (d.glog - 2);
             return;
