@@ -237,7 +237,8 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
     // 0.633 -> 0.678 ms, hence the bound).
     static const bool wide = !(std::getenv("PASE_2S_WIDE") && std::getenv("PASE_2S_WIDE")[0] == '0');
     const bool big = d.nout * d.K >= kMin2S;
-    if (single && (big || (wide && d.glog == 2 && d.K >= 128)) && (d.glog == 2 || d.glog == 3) && NSd <= 2) {
+    static const int max2s = std::getenv("PASE_2S_MAXG") ? std::atoi(std::getenv("PASE_2S_MAXG")) : 5;
+    if (single && (big || (wide && d.glog == 2 && d.K >= 128)) && NSd <= 2 && d.glog <= max2s) {
         for (const auto& cq : cand) {
             const int q2 = cq.second, f2 = cq.first;
             const int nb = d.tstar - f2 - 1;
@@ -249,7 +250,7 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
             const int form = NSd == 1 ? nb : (tv[d.tstar + 1].stride[d.qstar] != 0 ? 3 : 2);
             if (!big) d.glog = 3;
             set_tile2(d, q2, f2);
-            d.shape = pase::kShape2S + ((f2 - 1) * 4 + form) * 2 + (d.glog - 2);
+            d.shape = pase::kShape2S + ((f2 - 1) * 4 + form) * 4 + (d.glog - 2);
             return;
         }
     }
@@ -376,6 +377,22 @@ pase_status prepare(pase_ctx* ctx, bool device) {
 
     ctx->vd.assign(n, VertexDesc{});
     ctx->td.clear();
+    // critical vertices (by candidates): the longest candidate-weighted path from a leaf to the
+    // root through i is >= 90 % of the longest overall.  Only those widen their lane groups
+    // below (a vertex running beside many others widened loses throughput for nothing)
+    std::vector<char> critical(n, 0);
+    {
+        std::vector<double> w(n), top(n), bot(n);
+        for (int i = 0; i < n; ++i) w[i] = (double)P.tsize[i] * (double)P.K[P.sigma[i]];
+        for (int i = 0; i < n; ++i) {                       // children have lower ranks
+            double mx = 0.0;
+            for (int j : P.children[i]) mx = std::max(mx, top[j]);
+            top[i] = w[i] + mx;
+        }
+        for (int i = n - 1; i >= 0; --i) bot[i] = w[i] + (P.parent[i] >= 0 ? bot[P.parent[i]] : 0.0);
+        const double cp = top[n - 1];
+        for (int i = 0; i < n; ++i) critical[i] = top[i] + bot[i] - w[i] >= 0.9 * cp;
+    }
     for (int i = 0; i < n; ++i) {
         const int v = P.sigma[i];
         VertexDesc& d = ctx->vd[i];
@@ -473,6 +490,19 @@ pase_status prepare(pase_ctx* ctx, bool device) {
             }
             d.shape = (NP - 1) * 16 + NS * 4 + (d.glog - 2);
             if (d.wlog == 0 && !no_2d()) try_tile2(ctx, d, tv, top);
+            // a big vertex whose one-round tasks would not fill the grid widens its lane groups
+            // (all tile families encode log2 G in the shape's low 2 bits) until they do: its
+            // tasks then run K/G serial iterations in parallel on every CTA instead of twice as
+            // many on half of them
+            static const bool widen = !(std::getenv("PASE_WIDEN") && std::getenv("PASE_WIDEN")[0] == '0');
+            if (widen && critical[i] && d.shape >= 0 && d.wlog == 0 && d.nout * d.K >= kMin2S) {
+                const int64_t items = std::max<int64_t>(1, d.nitems / (d.part ? ctx->world : 1));
+                while (d.glog < 5 && (16 << d.glog) <= d.K &&
+                       (items * (int64_t(1) << d.glog) + 255) / 256 < ctx->nblocks) {
+                    ++d.glog;
+                    d.shape = (d.shape & ~3) | (d.glog - 2);
+                }
+            }
         } else {                                          // generic kernel
             d.glog = d.K <= 4 ? 2 : d.K <= 8 ? 3 : d.K <= 16 ? 4 : 5;
             d.shape = -1;

@@ -748,18 +748,19 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
         PASE_CASE2(2, 2) PASE_CASE2(2, 3) PASE_CASE2(2, 4) PASE_CASE2(2, 5)
 #undef PASE_CASE2
 #define PASE_CASE2S(NP0, FORM, NB, NS2, LGG)                                                      \
-    case kShape2S + ((NP0 - 1) * 4 + FORM) * 2 + (LGG - 2): {                                     \
+    case kShape2S + ((NP0 - 1) * 4 + FORM) * 4 + (LGG - 2): {                                     \
         constexpr int G_ = 1 << LGG, GPW_ = 32 / G_;                                              \
         tile2s_items<NP0, NB, NS2, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1);     \
         return;                                                                                   \
     }
+#define PASE_2S_G(NP0, FORM, NB, NS2)                                                             \
+        PASE_CASE2S(NP0, FORM, NB, NS2, 2) PASE_CASE2S(NP0, FORM, NB, NS2, 3)                     \
+        PASE_CASE2S(NP0, FORM, NB, NS2, 4) PASE_CASE2S(NP0, FORM, NB, NS2, 5)
 #define PASE_2S_FORMS(NP0)                                                                        \
-        PASE_CASE2S(NP0, 0, 0, 0, 2) PASE_CASE2S(NP0, 0, 0, 0, 3)                                 \
-        PASE_CASE2S(NP0, 1, 1, 0, 2) PASE_CASE2S(NP0, 1, 1, 0, 3)                                 \
-        PASE_CASE2S(NP0, 2, 0, 1, 2) PASE_CASE2S(NP0, 2, 0, 1, 3)                                 \
-        PASE_CASE2S(NP0, 3, 0, 2, 2) PASE_CASE2S(NP0, 3, 0, 2, 3)
+        PASE_2S_G(NP0, 0, 0, 0) PASE_2S_G(NP0, 1, 1, 0) PASE_2S_G(NP0, 2, 0, 1) PASE_2S_G(NP0, 3, 0, 2)
         PASE_2S_FORMS(1) PASE_2S_FORMS(2) PASE_2S_FORMS(3)
 #undef PASE_2S_FORMS
+#undef PASE_2S_G
 #undef PASE_CASE2S
         default: {
             const int gpw = 32 >> vd.glog;
@@ -898,7 +899,10 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
         __syncthreads();
         task = s_task;
         if (task < 0) break;                                // timed out (reported via *err)
-        run_shape(vd.shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1, red_b, red_c);
+        // wave-tail tasks (schedule.cpp) run the vertex's tile with wider lane groups: every
+        // tile family encodes log2(G) - 2 in the shape's low 2 bits
+        const int shape = tk.glog ? ((vd.shape & ~3) | (tk.glog - 2)) : vd.shape;
+        run_shape(shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1, red_b, red_c);
         int64_t t_comp = 0, t_sync = 0;
         if (trace && threadIdx.x == 0) t_comp = (int64_t)globaltimer();
         __syncthreads();                                    // task's stores precede the release

@@ -118,7 +118,8 @@ constexpr int kSchedLine = 32;   // int32 words per 128-B line (scheduler contro
 constexpr int kMaxTermsSh = 8;   // terms staged in shared memory (tiled shapes use <= 7)
 
 struct TaskDesc {            // persistent schedule: item range [i0, i1) of vertex vtx
-    int32_t vtx, pad;
+    int32_t vtx;
+    int32_t glog;            // 0: the vertex's lane groups; else log2 lanes per item (wave tail)
     int64_t i0, i1;
 };
 
@@ -145,7 +146,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
 constexpr int kTile = 8;     // max outputs per lane group along qstar
 constexpr int kTile1 = 4, kTile2 = 4;   // 2-D tile: outputs along qstar x q2
 constexpr int kShape2D = 64;            // shapes >= kShape2D: 2-D tiled (NS-1)*4 + (glog-2)
-constexpr int kShape2S = 96;            // shapes >= kShape2S: 2-D single-suffix ((NP0-1)*4 + form)*2 + (glog-2)
+constexpr int kShape2S = 96;            // shapes >= kShape2S: 2-D single-suffix ((NP0-1)*4 + form)*4 + (glog-2)
 //   form 0: P1 = [A], S = [S1]; 1: P1 = [A, B], S = [S1]; 2: S = [S1, const]; 3: S = [S1, S2 on q1]
 constexpr int kMaxP0 = 4, kMaxP1 = 2;   // 2-D tile: max scalar-prefix / q2-prefix terms
 constexpr int kCostRows = 64;  // edge-table rows per cost-table CTA

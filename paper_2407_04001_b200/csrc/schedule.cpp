@@ -27,6 +27,8 @@
 
 namespace pase {
 
+static const bool kWaveTail = !(std::getenv("PASE_WAVE_TAIL") && std::getenv("PASE_WAVE_TAIL")[0] == '0');
+
 pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world, int rank, int nblocks,
                            SchedPlan& out, std::string& err) {
     const int n = P.n;
@@ -35,7 +37,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     const int64_t spread = (int64_t)kTasksPerBlock * nblocks;
     const auto tt0 = std::chrono::steady_clock::now();
     // ---- per (vertex, rank): unit runs, split into tasks
-    struct GTask { int32_t rank, vtx; int64_t i0, i1; };
+    struct GTask { int32_t rank, vtx; int64_t i0, i1; int32_t glog; };   // glog 0 = the vertex's
     std::vector<GTask> all;
     std::vector<std::vector<std::vector<int32_t>>> tasks_of(n, std::vector<std::vector<int32_t>>(G));
     for (int i = 0; i < n; ++i) {
@@ -63,10 +65,30 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
             for (auto& r : runs) local += r.second - r.first;
             int64_t ti = std::max<int64_t>(groups, (local + spread - 1) / spread);
             ti = (ti + groups - 1) / groups * groups;
+            // wave tail: a vertex of one-round tasks spanning more than one wave of
+            // the grid leaves a partial last wave whose tasks take as long as full ones.  Those
+            // items go to tasks with wider lane groups (the largest G' <= 32 that still fits
+            // them in one wave, keeping >= 8 values of C per lane): K/G' serial iterations
+            // instead of K/G.  Same items, same results.
+            int64_t bulk_end = -1;
+            int32_t tail_glog = 0;
+            if (kWaveTail && runs.size() == 1 && d.shape >= 0 && d.wlog == 0 && d.glog < 5 && ti == groups) {
+                const int64_t T = (local + ti - 1) / ti;
+                if (T > nblocks && T % nblocks != 0) {
+                    const int64_t bulk = (T / nblocks) * nblocks * ti;
+                    const int64_t tail = local - bulk;
+                    int g2 = d.glog;
+                    while (g2 < 5 && (16 << g2) <= d.K && tail * (int64_t(2) << g2) <= (int64_t)nblocks * 256) ++g2;
+                    if (g2 > d.glog) { bulk_end = runs[0].first + bulk; tail_glog = g2; }
+                }
+            }
             for (auto& r : runs)
-                for (int64_t a = r.first; a < r.second; a += ti) {
+                for (int64_t a = r.first; a < r.second;) {
+                    const bool tail = bulk_end >= 0 && a >= bulk_end;
+                    const int64_t len = tail ? (256 >> tail_glog) : ti;
                     tasks_of[i][q].push_back((int32_t)all.size());
-                    all.push_back({q, i, a, std::min(r.second, a + ti)});
+                    all.push_back({q, i, a, std::min(r.second, a + len), tail ? tail_glog : 0});
+                    a += len;
                 }
         }
     }
@@ -109,7 +131,8 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     for (int64_t t = 0; t < ntk; ++t) {
         const VertexDesc& d = vd[all[t].vtx];
         const double cand = (double)(all[t].i1 - all[t].i0) * d.K * (d.shape < 0 ? 1 : d.q2 >= 0 ? kTile1 * kTile2 : kTile);
-        tdur[t] = 3.0 + cand / 3000.0;
+        const double lanes = all[t].glog ? (double)(1 << (all[t].glog - d.glog)) : 1.0;   // wave tail
+        tdur[t] = 3.0 + cand / (3000.0 * lanes);
     }
     for (int i = n - 1; i >= 0; --i) {                 // parents have higher ranks
         double work = 0.0, longest = 0.0;
@@ -188,7 +211,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         vd[i].task0 = (int32_t)out.tasks.size();
         for (int32_t t : tasks_of[i][rank]) {
             local_id[t] = (int32_t)out.tasks.size();
-            out.tasks.push_back({i, 0, all[t].i0, all[t].i1});
+            out.tasks.push_back({i, all[t].glog, all[t].i0, all[t].i1});
         }
         vd[i].ntasks = (int32_t)tasks_of[i][rank].size();
     }
