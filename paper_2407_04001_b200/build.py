@@ -35,18 +35,40 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = SO, defines=()) -> str:
-    """Build libpase.so; `out` / `defines` build an A/B variant next to it (tuning only)."""
+    """Build libpase.so; `out` / `defines` build an A/B variant next to it (tuning only).
+    Sources compile in parallel (one nvcc per file, device code with --split-compile), then
+    one nvcc link."""
     if not force and out == SO and not _stale():
         return SO
-    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-o", out + ".tmp",
-           *[os.path.join(CSRC, f) for f in SOURCES], "-ldl"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    import concurrent.futures as cf
+    import tempfile
+    tmp = tempfile.mkdtemp(prefix="pase_build_")
+    flags = [*NVCC_FLAGS, *[f"-D{d}" for d in defines]]
+
+    def compile_one(src):
+        obj = os.path.join(tmp, os.path.splitext(src)[0] + ".o")
+        extra = ["--split-compile=0"] if src.endswith(".cu") else []
+        r = subprocess.run([NVCC, *flags, *extra, "-c", os.path.join(CSRC, src), "-o", obj],
+                           capture_output=True, text=True)
+        return src, obj, r
+
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for src, obj, r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc build of {src} failed")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    r = subprocess.run([NVCC, *flags, "-shared", "-o", out + ".tmp", *[o for _, o, _ in results], "-ldl"],
+                       capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc build of libpase.so failed")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc link of libpase.so failed")
     os.replace(out + ".tmp", out)
+    for _, o, _ in results:
+        os.remove(o)
+    os.rmdir(tmp)
     return out
 
 
