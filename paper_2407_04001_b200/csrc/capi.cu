@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <new>
 #include <string>
@@ -33,6 +34,7 @@ struct pase_ctx {
     bool own_stream = false;
     bool async_pools = false;               // pools from the library's stream-ordered mempool
     bool big_pinned = false;                // h_total came from cudaMallocHost, not the cache
+    void* stage_block = nullptr;            // pinned upload image, returned after create's sync
     std::vector<cudaStream_t> aux;          // fork streams (per-vertex launch schedule)
     // pool 1: inputs, cost tables, DP tables (T/A written by peers), descriptors
     void* pool = nullptr;
@@ -136,6 +138,7 @@ cudaMemPool_t device_mempool(int dev) {
 // cache: cudaMallocHost/cudaFreeHost cost milliseconds (and cudaFreeHost synchronises).
 constexpr size_t kPinnedBlock = 64 << 10;
 std::vector<void*> g_pinned_free;
+std::map<void*, size_t> g_stage_size;
 
 void* pinned_get(size_t bytes, bool* big) {
     *big = bytes > kPinnedBlock;
@@ -150,6 +153,33 @@ void* pinned_get(size_t bytes, bool* big) {
     void* p = nullptr;
     if (cudaMallocHost(&p, *big ? bytes : kPinnedBlock) != cudaSuccess) return nullptr;
     return p;
+}
+
+// Pinned upload staging blocks (pase_create): recycled, grown to the largest request.
+std::vector<std::pair<void*, size_t>> g_stage_free;
+
+void* stage_get(size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (size_t k = 0; k < g_stage_free.size(); ++k)
+            if (g_stage_free[k].second >= bytes) {
+                void* p = g_stage_free[k].first;
+                g_stage_free.erase(g_stage_free.begin() + k);
+                return p;
+            }
+    }
+    const size_t sz = std::max<size_t>(bytes, 4 << 20);
+    void* p = nullptr;
+    if (cudaMallocHost(&p, sz) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_stage_size[p] = sz;
+    return p;
+}
+
+void stage_put(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_stage_free.push_back({p, g_stage_size[p]});
 }
 
 void pinned_put(void* p, bool big) {
@@ -560,14 +590,21 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     }
     ctx->nbtlev = nlev;
     // one host image per pool (the uploaded prefix), one copy each
-    auto stage = [](std::vector<char>& img, void* pool, void* dst, const void* src, size_t bytes) {
-        const size_t off = (size_t)((char*)dst - (char*)pool);
-        if (off + bytes > img.size()) img.resize(off + bytes);
-        if (bytes) std::memcpy(img.data() + off, src, bytes);
+    // one upload image per pool (the uploaded prefix of each), staged in PINNED host memory
+    // (a recycled process-wide block) so both copies run asynchronously at full PCIe rate;
+    // host-only contexts only size them
+    const size_t size1 = (size_t)((char*)ctx->d_L - (char*)ctx->pool);
+    const size_t size2 = (size_t)((char*)ctx->d_sched - (char*)ctx->pool2);
+    ctx->h2d_bytes = size1 + size2;
+    if (!device) return PASE_OK;
+    char* img = (char*)stage_get(size1 + size2);
+    if (!img) { ctx->err = "cudaMallocHost of the upload image failed"; return PASE_ERR_RESOURCE; }
+    ctx->stage_block = img;
+    auto stage = [&](char* base, void* pool, void* dst, const void* src, size_t bytes) {
+        if (bytes) std::memcpy(base + ((char*)dst - (char*)pool), src, bytes);
     };
-    std::vector<char> img1, img2;
-    img1.reserve((size_t)((char*)ctx->d_L - (char*)ctx->pool));
-    img2.reserve((size_t)((char*)ctx->d_sched - (char*)ctx->pool2));
+    char* img1 = img;
+    char* img2 = img + size1;
     stage(img1, ctx->pool, ctx->d_nodes, P.nodes.data(), sizeof(pase_node) * n);
     stage(img1, ctx->pool, ctx->d_K, P.K.data(), sizeof(int32_t) * n);
     stage(img1, ctx->pool, ctx->d_cfg_off, P.cfg_off.data(), sizeof(int64_t) * (n + 1));
@@ -582,11 +619,9 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     stage(img2, ctx->pool2, ctx->d_sched_init, sched.data(), ctx->sched_bytes);
     stage(img2, ctx->pool2, ctx->d_tasks, ctx->sp.tasks.data(), sizeof(pase::TaskDesc) * ctx->sp.tasks.size());
     stage(img2, ctx->pool2, ctx->d_order, ctx->sp.order.data(), sizeof(int32_t) * ctx->sp.order.size());
-    ctx->h2d_bytes = img1.size() + img2.size();
-    if (!device) return PASE_OK;
-    // pageable sources: the calls return once the images are staged, so they may go out of scope
-    CUDA_TRY(cudaMemcpyAsync(ctx->pool, img1.data(), img1.size(), cudaMemcpyHostToDevice, ctx->stream));
-    CUDA_TRY(cudaMemcpyAsync(ctx->pool2, img2.data(), img2.size(), cudaMemcpyHostToDevice, ctx->stream));
+    // the block returns to the cache once pase_create has synchronised the stream
+    CUDA_TRY(cudaMemcpyAsync(ctx->pool, img1, size1, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx->pool2, img2, size2, cudaMemcpyHostToDevice, ctx->stream));
     CUDA_TRY(cudaMemsetAsync(ctx->d_bar, 0, sizeof(int32_t) * 3 * pase::kSchedLine, ctx->stream));
     return PASE_OK;
 }
@@ -825,6 +860,8 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
     // the pools are complete before any other stream (a peer's, the legacy one used by the
     // introspection hooks) touches them
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) { ctx->err = "cudaStreamSynchronize failed"; return fail(PASE_ERR_CUDA); }
+    stage_put(ctx->stage_block);
+    ctx->stage_block = nullptr;
     auto t_graph = std::chrono::steady_clock::now();
     fill_stats(ctx);
     using ms = std::chrono::duration<double, std::milli>;
@@ -1026,7 +1063,8 @@ void pase_destroy(pase_ctx* ctx) {
     if (!ctx) return;
     if (ctx->dev < 0) { delete ctx; return; }
     cudaSetDevice(ctx->dev);
-    if (ctx->launched && ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if ((ctx->launched || ctx->stage_block) && ctx->stream) cudaStreamSynchronize(ctx->stream);
+    stage_put(ctx->stage_block);                // failed create: upload image back to the cache
     if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
     for (auto s : ctx->aux) cudaStreamDestroy(s);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
