@@ -272,7 +272,21 @@ def main():
                "steps": len(a_ms), "ms_per_step": a_tot / len(a_ms), "dp_fill_ms": statistics.mean(a_dp),
                "candidates": int(ast["candidates"]), "dp_fp64_ops": int(ast["dp_fp64_ops"])}
 
-    # e2e through the public API with host inputs (create + solve + destroy per step)
+    # e2e through the public API with host inputs (create + solve + destroy per step): the
+    # graph is held in the C ABI's input layout (pase.Graph: pase_graph node / edge arrays in
+    # host memory, converted from the dict once), so each step runs pase_create from host
+    # arrays (ingest, plan, H2D upload), pase_solve (strategy D2H) and pase_destroy
+    c_graph = pase.Graph(graph)
+
+    def make_ctx_host():
+        c = pase.Context(c_graph, p, policy=policy, device=device, stream=stream.cuda_stream,
+                         rank=rank, world=world, virtual_ranks=share)
+        if world > 1:
+            hs = [None] * world
+            dist.all_gather_object(hs, c.export_handle())
+            c.connect(hs)
+        return c
+
     e2e_ms = []
     for i in range(args.e2e_steps + 1):
         with torch.cuda.stream(stream):
@@ -280,7 +294,7 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        with make_ctx() as c2:
+        with make_ctx_host() as c2:
             c2.solve()
         e1.record(stream)
         e1.synchronize()
@@ -341,7 +355,7 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "entries/s", "h2d_bytes_per_step": int(st["h2d_bytes"]),
                 "d2h_bytes_per_step": int(st["d2h_bytes"]), "ms_per_step": e2e_tot / max(len(e2e_ms), 1),
-                "what": "pase_create (host graph -> plan -> H2D) + pase_solve (D2H strategy) + pase_destroy"},
+                "what": "pase_create (host pase_graph arrays -> plan -> pinned H2D) + pase_solve (D2H strategy) + pase_destroy"},
         "throughput_regime": alt,
         "gpu_launches": int(st["n_launches"]) * args.steps,
         "clocks": clocks,

@@ -153,54 +153,67 @@ def _ptr(a: np.ndarray, ct):
 
 def marshal_graph(graph: dict):
     """dict -> (pase_graph, keepalive).  Layout per include/pase.h; the node/edge arrays are
-    numpy structured arrays with the ctypes structs' dtype (one vectorised fill per field)."""
+    numpy structured arrays with the ctypes structs' dtype, filled from one int64 matrix
+    (one row of every integer field per node, one array conversion)."""
     nodes = graph["nodes"]
     edges = graph["edges"]
     n, m = len(nodes), len(edges)
     NA = np.zeros(max(n, 1), dtype=np.dtype(pase_node))
-    Z8, Z4 = [0] * PASE_MAX_DIMS, [0] * PASE_MAX_HALO
-    cols = {k: [] for k in ("n_dims", "size", "splittable_mask", "n_out_axes", "out_axes", "n_w_axes",
-                            "w_axes", "flop_dims_mask", "flops_per_point", "n_halo", "halo_spatial",
-                            "halo_filter", "elem_bytes")}
+    D, HL = PASE_MAX_DIMS, PASE_MAX_HALO
+    Z8, Z4 = [0] * D, [0] * HL
+    rows = []
     for v, nd in enumerate(nodes):
         if nd["id"] != v:
             raise ValueError(f"node {v}: id {nd['id']} must equal its index")
         dims = nd["dims"]
-        if len(dims) > PASE_MAX_DIMS:
-            raise ValueError(f"node {v}: more than {PASE_MAX_DIMS} dims")
-        oa = list(nd["out_axes"])
-        w = list(nd.get("w_axes") or [])
+        nd_ = len(dims)
+        if nd_ > D:
+            raise ValueError(f"node {v}: more than {D} dims")
+        oa = nd["out_axes"]
+        w = nd.get("w_axes") or []
         fd = nd.get("flop_dims")
         halo = nd.get("halo") or []
-        if len(halo) > PASE_MAX_HALO:
-            raise ValueError(f"node {v}: more than {PASE_MAX_HALO} halo pairs")
-        cols["n_dims"].append(len(dims))
-        cols["size"].append([int(d["size"]) for d in dims] + Z8[len(dims):])
-        cols["splittable_mask"].append(sum(1 << k for k, d in enumerate(dims) if d.get("splittable", True)))
-        cols["n_out_axes"].append(len(oa))
-        cols["out_axes"].append(oa + Z8[len(oa):])
-        cols["n_w_axes"].append(len(w))
-        cols["w_axes"].append(w + Z8[len(w):])
-        cols["flop_dims_mask"].append(0 if fd is None else sum(1 << k for k in fd))
-        cols["flops_per_point"].append(int(nd.get("flops_per_point", 2)))
-        cols["n_halo"].append(len(halo))
-        cols["halo_spatial"].append([h for h, _ in halo] + Z4[len(halo):])
-        cols["halo_filter"].append([f for _, f in halo] + Z4[len(halo):])
-        cols["elem_bytes"].append(int(nd.get("elem_bytes", 4)))
+        if len(halo) > HL:
+            raise ValueError(f"node {v}: more than {HL} halo pairs")
+        mask = 0
+        sizes = []
+        for k, d in enumerate(dims):
+            sizes.append(d["size"])
+            if d.get("splittable", True):
+                mask |= 1 << k
+        fmask = 0
+        if fd is not None:
+            for k in fd:
+                fmask |= 1 << k
+        rows.append([nd_, *sizes, *Z8[nd_:], mask, len(oa), *oa, *Z8[len(oa):], len(w), *w, *Z8[len(w):],
+                     fmask, nd.get("flops_per_point", 2), len(halo), *[h for h, _ in halo], *Z4[len(halo):],
+                     *[f for _, f in halo], *Z4[len(halo):], nd.get("elem_bytes", 4)])
     if n:
-        for k, col in cols.items():
-            if col and isinstance(col[0], list):          # flatten rows: one array conversion
-                NA[k] = np.array([x for row in col for x in row], dtype=NA.dtype[k].base).reshape(n, -1)
-            else:
-                NA[k] = np.array(col, dtype=NA.dtype[k])
+        M = np.array(rows, dtype=np.int64)
+        c = 0
+        for k, width in (("n_dims", 1), ("size", D), ("splittable_mask", 1), ("n_out_axes", 1), ("out_axes", D),
+                         ("n_w_axes", 1), ("w_axes", D), ("flop_dims_mask", 1), ("flops_per_point", 1),
+                         ("n_halo", 1), ("halo_spatial", HL), ("halo_filter", HL), ("elem_bytes", 1)):
+            NA[k] = M[:, c] if width == 1 else M[:, c:c + width]
+            c += width
     EA = np.zeros(max(m, 1), dtype=np.dtype(pase_edge))
     if m:
-        EA["src"] = [ed["src"] for ed in edges]
-        EA["dst"] = [ed["dst"] for ed in edges]
-        EA["axis_map"] = np.array([x for ed in edges for x in list(ed["axis_map"]) + [-1] * (PASE_MAX_DIMS - len(ed["axis_map"]))],
-                                  dtype=np.int32).reshape(m, PASE_MAX_DIMS)
+        E = np.array([[ed["src"], ed["dst"], *ed["axis_map"], *[-1] * (D - len(ed["axis_map"]))] for ed in edges],
+                     dtype=np.int64)
+        EA["src"] = E[:, 0]
+        EA["dst"] = E[:, 1]
+        EA["axis_map"] = E[:, 2:]
     g = pase_graph(n, NA.ctypes.data_as(C.POINTER(pase_node)), m, EA.ctypes.data_as(C.POINTER(pase_edge)))
     return g, (NA, EA)
+
+
+class Graph:
+    """A graph already in the C ABI's input layout (pase_graph + node / edge arrays): marshal a
+    dict once, then create any number of contexts from it (Context accepts a Graph or a dict)."""
+
+    def __init__(self, graph: dict):
+        self.graph = graph
+        self.c_graph, self._keep = marshal_graph(graph)
 
 
 def make_machine(flops: float = 1e13, bandwidth: float = 1e10, policy: int = PASE_CFG_EXACT_P,
@@ -231,9 +244,12 @@ class Context:
         flops = flops if flops is not None else mach_d.get("flops", 1e13)
         bandwidth = bandwidth if bandwidth is not None else mach_d.get("bandwidth", 1e10)
         pol = POLICIES[policy] if isinstance(policy, str) else int(policy)
+        if isinstance(graph, Graph):
+            g, self._keep, graph = graph.c_graph, graph._keep, graph.graph
+        else:
+            g, self._keep = marshal_graph(graph)
         self.graph = graph
         self.n, self.m, self.p = len(graph["nodes"]), len(graph["edges"]), int(p)
-        g, self._keep = marshal_graph(graph)
         order = ORDERINGS[ordering] if isinstance(ordering, str) else int(ordering)
         self._mach = make_machine(flops, bandwidth, pol, device, stream, rank, world, virtual_ranks,
                                   table_budget, redundant_below, order)

@@ -182,3 +182,18 @@ def test_bfs_ordering_oom_on_inception(lib):
     assert ei.value.status == 2 and "K =" in str(ei.value)
     ctx = pase.Context(g, 8, device=-1)
     assert ctx.stats()["table_entries"] * 10 < 1e9
+
+
+def test_premarshalled_graph_same_plan(lib):
+    """pase.Graph (the C ABI input layout, marshalled once) plans exactly like the dict."""
+    g, p = zoo.bench_graph("transformer")
+    G = pase.Graph(g)
+    a = pase.Context(g, p, device=-1)
+    for _ in range(2):
+        b = pase.Context(G, p, device=-1)
+        sa, da, pa = a.order()
+        sb, db, pb = b.order()
+        assert list(sa) == list(sb) and list(pa) == list(pb)
+        assert np.array_equal(a.K(), b.K())
+        b.close()
+    a.close()
