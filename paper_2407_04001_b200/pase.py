@@ -235,17 +235,20 @@ def make_machine(flops: float = 1e13, bandwidth: float = 1e10, policy: int = PAS
 class Context:
     """Owns one pase_ctx (pase_create ... pase_destroy)."""
 
-    def __init__(self, graph: dict, p: int, policy="exact_p", flops: Optional[float] = None,
+    def __init__(self, graph, p: int, policy="exact_p", flops: Optional[float] = None,
                  bandwidth: Optional[float] = None, device: int = 0, stream: Optional[int] = None,
                  rank: int = 0, world: int = 1, virtual_ranks: bool = False, table_budget: int = 0,
                  redundant_below: int = 4 << 20, ordering="sortnodes"):
         L = load()
+        G = graph if isinstance(graph, Graph) else None
+        if G is not None:
+            graph = G.graph
         mach_d = graph.get("machine") or {}
         flops = flops if flops is not None else mach_d.get("flops", 1e13)
         bandwidth = bandwidth if bandwidth is not None else mach_d.get("bandwidth", 1e10)
         pol = POLICIES[policy] if isinstance(policy, str) else int(policy)
-        if isinstance(graph, Graph):
-            g, self._keep, graph = graph.c_graph, graph._keep, graph.graph
+        if G is not None:
+            g, self._keep = G.c_graph, G._keep
         else:
             g, self._keep = marshal_graph(graph)
         self.graph = graph
