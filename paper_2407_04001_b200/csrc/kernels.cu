@@ -31,8 +31,8 @@ __device__ __forceinline__ double d_allreduce(int64_t g, int64_t bytes) {
 
 // t_l (DESIGN reading I): FLOPs of one (equal) shard + r * (reduction AR + gradient AR + halo)
 __device__ double d_layer_cost(const pase_node& x, const int32_t* c, double r) {
-    int64_t s[kMaxDims];
-    for (int k = 0; k < x.n_dims; ++k) s[k] = x.size[k] / c[k];
+    int64_t s[kMaxDims];                       // sizes < 2^31 (validated): 32-bit divisions
+    for (int k = 0; k < x.n_dims; ++k) s[k] = (int64_t)((uint32_t)x.size[k] / (uint32_t)c[k]);
     int64_t compute = x.flops_per_point;
     for (int k = 0; k < x.n_dims; ++k)
         if (x.flop_dims_mask == 0u || (x.flop_dims_mask >> k & 1u)) compute *= s[k];
@@ -96,14 +96,17 @@ cost_tables_kernel(const pase_node* __restrict__ nodes, const int32_t* __restric
     const uint64_t elem2 = 2ull * (uint64_t)u.elem_bytes;
     // t_x (DESIGN reading K): per output axis a of src, held_a = ext / c_src, need_a =
     // ceil(ext / c_dst[map_a]) (ext if unmapped); t_x = 2 elem (prod need - prod min(need, held))
+    // (sizes < 2^31, validated on the host: 32-bit divisions)
+    const int32_t* cfg_s = cfg + cfg_off[e.src] * kMaxDims;
+    const int32_t* cfg_d = cfg + cfg_off[e.dst] * kMaxDims;
     auto held = [&](int cs, int a) -> uint32_t {
-        const int32_t* c = cfg + (cfg_off[e.src] + cs) * kMaxDims;
-        return (uint32_t)(u.size[u.out_axes[a]] / c[u.out_axes[a]]);
+        const int32_t* c = cfg_s + cs * kMaxDims;
+        return (uint32_t)u.size[u.out_axes[a]] / (uint32_t)c[u.out_axes[a]];
     };
     auto need = [&](int cd, int a) -> uint32_t {
-        const int32_t* c = cfg + (cfg_off[e.dst] + cd) * kMaxDims;
-        const int64_t ext = u.size[u.out_axes[a]];
-        return (uint32_t)(e.axis_map[a] < 0 ? ext : (ext + c[e.axis_map[a]] - 1) / c[e.axis_map[a]]);
+        const int32_t* c = cfg_d + cd * kMaxDims;
+        const uint32_t ext = (uint32_t)u.size[u.out_axes[a]];
+        return e.axis_map[a] < 0 ? ext : (ext + (uint32_t)c[e.axis_map[a]] - 1u) / (uint32_t)c[e.axis_map[a]];
     };
     // rows = later endpoint: src configs (held) if later_is_src, else dst configs (need)
     for (int rr = threadIdx.x; rr < ch.nrows; rr += blockDim.x) {
