@@ -196,9 +196,9 @@ std::vector<pase::CostChunk> cost_chunks(const Plan& P) {
         const pase_edge& x = P.edges[e];
         const int late = P.rank[x.src] > P.rank[x.dst] ? x.src : x.dst;
         for (int r0 = 0; r0 < P.K[late]; r0 += pase::kCostRows)
-            ch.push_back({P.n + e, r0, std::min(pase::kCostRows, P.K[late] - r0), 0});
+            ch.push_back({P.n + e, r0, std::min(pase::kCostRows, P.K[late] - r0), x.src});
     }
-    for (int v = 0; v < P.n; ++v) ch.push_back({v, 0, P.K[v], 0});
+    for (int v = 0; v < P.n; ++v) ch.push_back({v, 0, P.K[v], v});
     return ch;
 }
 

@@ -29,21 +29,32 @@ __device__ __forceinline__ double d_allreduce(int64_t g, int64_t bytes) {
     return __ddiv_rn(__ull2double_rn((unsigned long long)(2 * (g - 1) * bytes)), __ll2double_rn(g));
 }
 
-// t_l (DESIGN reading I): FLOPs of one (equal) shard + r * (reduction AR + gradient AR + halo)
-__device__ double d_layer_cost(const pase_node& x, const int32_t* c, double r) {
-    int64_t s[kMaxDims];                       // sizes < 2^31 (validated): 32-bit divisions
-    for (int k = 0; k < x.n_dims; ++k) s[k] = (int64_t)((uint32_t)x.size[k] / (uint32_t)c[k]);
-    int64_t compute = x.flops_per_point;
-    for (int k = 0; k < x.n_dims; ++k)
-        if (x.flop_dims_mask == 0u || (x.flop_dims_mask >> k & 1u)) compute *= s[k];
+// t_l (DESIGN reading I): FLOPs of one (equal) shard + r * (reduction AR + gradient AR + halo).
+// The node lives in shared memory; every per-dim array is indexed by compile-time k (fully
+// unrolled over kMaxDims, so they stay in registers) and the axis lists become dim masks
+// (axes are distinct, so the products are the same integers in any order).
+__device__ double d_layer_cost(const pase_node& x, const int32_t* __restrict__ c, double r) {
+    int32_t cc[kMaxDims];
+    {
+        const int4 lo = *reinterpret_cast<const int4*>(c), hi = *reinterpret_cast<const int4*>(c + 4);
+        cc[0] = lo.x; cc[1] = lo.y; cc[2] = lo.z; cc[3] = lo.w; cc[4] = hi.x; cc[5] = hi.y; cc[6] = hi.z; cc[7] = hi.w;
+    }
+    const int nd = x.n_dims;
     uint32_t out_m = 0, w_m = 0;
-    int64_t out_elems = 1, w_elems = 1;
-    for (int a = 0; a < x.n_out_axes; ++a) { out_m |= 1u << x.out_axes[a]; out_elems *= s[x.out_axes[a]]; }
-    for (int a = 0; a < x.n_w_axes; ++a) { w_m |= 1u << x.w_axes[a]; w_elems *= s[x.w_axes[a]]; }
-    int64_t g_red = 1, g_grad = 1;
-    for (int k = 0; k < x.n_dims; ++k) {
-        if (!(out_m >> k & 1u)) g_red *= c[k];
-        if (!(w_m >> k & 1u)) g_grad *= c[k];
+    for (int a = 0; a < x.n_out_axes; ++a) out_m |= 1u << x.out_axes[a];
+    for (int a = 0; a < x.n_w_axes; ++a) w_m |= 1u << x.w_axes[a];
+    const uint32_t fl_m = x.flop_dims_mask == 0u ? 0xffu : x.flop_dims_mask;
+    int64_t s[kMaxDims];                       // sizes < 2^31 (validated): 32-bit divisions
+    int64_t compute = x.flops_per_point, out_elems = 1, w_elems = 1, g_red = 1, g_grad = 1;
+#pragma unroll
+    for (int k = 0; k < kMaxDims; ++k) {
+        const bool in = k < nd;
+        s[k] = in ? (int64_t)((uint32_t)x.size[k] / (uint32_t)cc[k]) : 1;
+        if (in && (fl_m >> k & 1u)) compute *= s[k];
+        if (out_m >> k & 1u) out_elems *= s[k];
+        if (w_m >> k & 1u) w_elems *= s[k];
+        if (in && !(out_m >> k & 1u)) g_red *= cc[k];
+        if (in && !(w_m >> k & 1u)) g_grad *= cc[k];
     }
     const int64_t out_bytes = (int64_t)x.elem_bytes * out_elems;
     const int64_t w_bytes = x.n_w_axes > 0 ? (int64_t)x.elem_bytes * w_elems : 0;
@@ -51,17 +62,28 @@ __device__ double d_layer_cost(const pase_node& x, const int32_t* c, double r) {
     int64_t halo = 0;
     for (int q = 0; q < x.n_halo; ++q) {
         const int h = x.halo_spatial[q], f = x.halo_filter[q];
-        if (c[h] > 1 && x.size[f] > 1) {
-            int64_t face = 1;
-            for (int a = 0; a < x.n_out_axes; ++a)
-                if (x.out_axes[a] != h) face *= s[x.out_axes[a]];
-            halo += 2 * (int64_t)x.elem_bytes * (x.size[f] - 1) * face;
+        int32_t ch = 1;
+        int64_t face = 1;
+#pragma unroll
+        for (int k = 0; k < kMaxDims; ++k) {
+            if (k == h) ch = cc[k];
+            if ((out_m >> k & 1u) && k != h) face *= s[k];
         }
+        if (ch > 1 && x.size[f] > 1) halo += 2 * (int64_t)x.elem_bytes * (x.size[f] - 1) * face;
     }
     double comm = d_allreduce(g_red, out_bytes);
     comm = __dadd_rn(comm, d_allreduce(g_grad, w_bytes));
     comm = __dadd_rn(comm, __ull2double_rn((unsigned long long)halo));
     return __dadd_rn(__ull2double_rn((unsigned long long)compute), __dmul_rn(r, comm));
+}
+
+// cooperative copy of a small struct into shared memory (4-byte words)
+template <typename T>
+__device__ __forceinline__ void stage_struct(T* dst, const T* src) {
+    static_assert(sizeof(T) % 4 == 0, "word copy");
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+    for (int w = threadIdx.x; w < (int)(sizeof(T) / 4); w += blockDim.x) d[w] = s[w];
 }
 
 // One CTA per chunk: a vertex (all K_v entries of L_v) or up to kCostRows rows of one
@@ -70,7 +92,7 @@ __device__ double d_layer_cost(const pase_node& x, const int32_t* c, double r) {
 // loop is a min / multiply per axis, and stores are coalesced along the column.
 constexpr int kCostCols = 512;
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 cost_tables_kernel(const pase_node* __restrict__ nodes, const int32_t* __restrict__ K,
                    const int64_t* __restrict__ cfg_off, const int32_t* __restrict__ cfg,
                    const int64_t* __restrict__ loff, int n, const EdgeDesc* __restrict__ edges,
@@ -81,15 +103,23 @@ cost_tables_kernel(const pase_node* __restrict__ nodes, const int32_t* __restric
     __shared__ uint32_t colq[kMaxDims][kCostCols];
     __shared__ uint64_t rowprod[kCostRows];
     __shared__ uint64_t colprod[kCostCols];
+    __shared__ pase_node su;                                // the vertex / the edge's producer
+    __shared__ EdgeDesc se;
     const CostChunk ch = chunks[blockIdx.x];
+    // chunk.node = the vertex, or the edge's src: both structs are staged in one round of loads
+    stage_struct(&su, nodes + ch.node);
+    if (ch.item >= n) stage_struct(&se, edges + (ch.item - n));
+    __syncthreads();
     if (ch.item < n) {
         const int v = ch.item;
-        for (int c = threadIdx.x; c < K[v]; c += blockDim.x)
-            L[loff[v] + c] = d_layer_cost(nodes[v], cfg + (cfg_off[v] + c) * kMaxDims, r);
+        const int Kv = K[v];
+        const int32_t* cv = cfg + cfg_off[v] * kMaxDims;
+        double* Lv = L + loff[v];
+        for (int c = threadIdx.x; c < Kv; c += blockDim.x) Lv[c] = d_layer_cost(su, cv + c * kMaxDims, r);
         return;
     }
-    const EdgeDesc& e = edges[ch.item - n];
-    const pase_node& u = nodes[e.src];
+    const EdgeDesc& e = se;
+    const pase_node& u = su;
     const int nax = u.n_out_axes;
     const int early = e.later_is_src ? e.dst : e.src;
     const int Ke = K[early];

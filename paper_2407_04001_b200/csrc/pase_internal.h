@@ -65,7 +65,7 @@ struct EdgeDesc {            // cost-table kernel: one per edge
 struct CostChunk {           // cost-table kernel work unit (one CTA)
     int32_t item;            // < n: vertex (all of L_v); >= n: edge item - n
     int32_t row0, nrows;     // edge: rows [row0, row0 + nrows) of W_e (later-endpoint configs)
-    int32_t pad;
+    int32_t node;            // the vertex, or the edge's src (staged with the edge descriptor)
 };
 
 struct TermDesc {            // one summand of Eq. 4 for a vertex (L, one W_e, or one child T_j)
