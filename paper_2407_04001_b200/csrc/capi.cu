@@ -72,6 +72,7 @@ struct pase_ctx {
     int ntasks = 0, nblocks = 0;
     int64_t total_tasks = 0;
     bool persistent = true;
+    bool cost_tasks = false;                // persistent: cost tables as tasks of the DP kernel
     // multi-GPU
     pase::Peers peers{};
     bool connected = false;
@@ -195,11 +196,30 @@ std::vector<pase::CostChunk> cost_chunks(const Plan& P) {
     for (int e = 0; e < P.m; ++e) {
         const pase_edge& x = P.edges[e];
         const int late = P.rank[x.src] > P.rank[x.dst] ? x.src : x.dst;
+        // W_e is read by its earlier-ranked endpoint (reading T)
+        const int reader = std::min(P.rank[x.src], P.rank[x.dst]);
         for (int r0 = 0; r0 < P.K[late]; r0 += pase::kCostRows)
-            ch.push_back({P.n + e, r0, std::min(pase::kCostRows, P.K[late] - r0), x.src});
+            ch.push_back({P.n + e, r0, std::min(pase::kCostRows, P.K[late] - r0), x.src, reader});
     }
-    for (int v = 0; v < P.n; ++v) ch.push_back({v, 0, P.K[v], v});
+    for (int v = 0; v < P.n; ++v) ch.push_back({v, 0, P.K[v], v, P.rank[v]});
     return ch;
+}
+
+pase::CostArgs cost_args(const pase_ctx* ctx) {
+    pase::CostArgs a{};
+    a.nodes = ctx->d_nodes;
+    a.K = ctx->d_K;
+    a.cfg_off = ctx->d_cfg_off;
+    a.cfg = ctx->d_cfg;
+    a.loff = ctx->d_loff;
+    a.n = ctx->P.n;
+    a.enabled = ctx->override_tables ? 0 : 1;
+    a.edges = ctx->d_edges;
+    a.chunks = ctx->d_chunks;
+    a.r = ctx->P.r;
+    a.L = ctx->d_L;
+    a.W = ctx->d_W;
+    return a;
 }
 
 bool trace_on() {
@@ -539,7 +559,10 @@ pase_status prepare(pase_ctx* ctx, bool device) {
         }
     }
     // tasks, broadcast flags, pending counters, claim order (schedule.cpp)
-    pase_status st = pase::build_schedule(P, ctx->vd, ctx->world, ctx->rank, ctx->nblocks, ctx->sp, ctx->err);
+    std::vector<int32_t> consumer(chunks.size());
+    for (size_t k = 0; k < chunks.size(); ++k) consumer[k] = chunks[k].consumer;
+    pase_status st = pase::build_schedule(P, ctx->vd, ctx->world, ctx->rank, ctx->nblocks, ctx->sp, ctx->err,
+                                          ctx->cost_tasks ? &consumer : nullptr);
     if (st) return st;
     ctx->ntasks = (int)ctx->sp.tasks.size();
     ctx->total_tasks = ctx->sp.total_tasks;
@@ -649,9 +672,9 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
     const unsigned ext = capture ? cudaEventRecordExternal : cudaEventRecordDefault;
     int32_t* d_err = ctx->d_err;
     CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int32_t), s));
-    if (!ctx->override_tables)
-        pase::launch_cost_tables(ctx->d_nodes, ctx->d_K, ctx->d_cfg_off, ctx->d_cfg, ctx->d_loff, n,
-                                 ctx->d_edges, ctx->d_chunks, ctx->nchunks, P.r, ctx->d_L, ctx->d_W, s);
+    // cost tables: tasks of the persistent kernel (the DP's first tasks overlap them); the
+    // per-vertex launch schedule runs them as their own kernel first
+    if (!ctx->override_tables && !ctx->cost_tasks) pase::launch_cost_tables(cost_args(ctx), ctx->nchunks, s);
     // phase split: external event nodes (plain records would only become capture edges)
     CUDA_TRY(cudaEventRecordWithFlags(ctx->ev_mid, s, ext));
     std::vector<char> used(nstreams, 0);
@@ -659,7 +682,8 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
         CUDA_TRY(cudaMemcpyAsync(ctx->d_sched, ctx->d_sched_init, ctx->sched_bytes, cudaMemcpyDeviceToDevice, s));
         if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, s);
         pase::launch_dp_persistent(ctx->d_vd, ctx->d_td, ctx->d_tasks, ctx->d_order, ctx->ntasks, ctx->d_sched,
-                                   d_err, ctx->peers, ctx->nblocks, trace_on() ? ctx->d_trace : nullptr, s);
+                                   d_err, ctx->peers, cost_args(ctx), ctx->nblocks,
+                                   trace_on() ? ctx->d_trace : nullptr, s);
         if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, s);
     } else {
         CUDA_TRY(cudaEventRecord(start, s));
@@ -705,7 +729,7 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
 // at every solve.
 pase_status record_graph(pase_ctx* ctx) {
     const int dp_launches = ctx->persistent ? 1 + (ctx->world > 1 ? 2 : 0) : ctx->P.n;
-    ctx->stats.n_launches = (ctx->override_tables ? 0 : 1) + dp_launches + 1;
+    ctx->stats.n_launches = (ctx->override_tables || ctx->cost_tasks ? 0 : 1) + dp_launches + 1;
     const char* ng = std::getenv("PASE_NO_GRAPH");
     ctx->no_graph = ng && ng[0] == '1';
     if (ctx->exec) { cudaGraphExecDestroy(ctx->exec); ctx->exec = nullptr; }
@@ -794,6 +818,11 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
     {
         const char* sc = std::getenv("PASE_SCHEDULE");
         ctx->persistent = !(sc && std::strcmp(sc, "launches") == 0) || ctx->world > 1;
+        // PASE_COST_TASKS=1: the cost tables run as tasks of the persistent DP kernel instead of
+        // their own kernel first (measured slower on Transformer p=64: 0.699 vs 0.682 ms per
+        // solve; neutral to 2 % faster elsewhere -- profiles/r01_ab_scheduling.txt)
+        const char* ct = std::getenv("PASE_COST_TASKS");
+        ctx->cost_tasks = ctx->persistent && ct && ct[0] == '1';
     }
     if (!device) {                          // host-only planning context (no device work)
         ctx->nblocks = std::max(1, 2 * 148 / (ctx->virtual_ranks ? ctx->world : 1));
@@ -1200,9 +1229,7 @@ namespace {
 pase_status eq1_prepare(pase_ctx* ctx, pase::EvalEdge** ed_dev) {
     const Plan& P = ctx->P;
     CUDA_TRY(cudaSetDevice(ctx->dev));
-    if (!ctx->override_tables)
-        pase::launch_cost_tables(ctx->d_nodes, ctx->d_K, ctx->d_cfg_off, ctx->d_cfg, ctx->d_loff, P.n,
-                                 ctx->d_edges, ctx->d_chunks, ctx->nchunks, P.r, ctx->d_L, ctx->d_W, ctx->stream);
+    if (!ctx->override_tables) pase::launch_cost_tables(cost_args(ctx), ctx->nchunks, ctx->stream);
     std::vector<pase::EvalEdge> ed(std::max(P.m, 1));
     for (int e = 0; e < P.m; ++e) {
         const pase_edge& x = P.edges[e];

@@ -89,46 +89,34 @@ __device__ __forceinline__ void stage_struct(T* dst, const T* src) {
 // One CTA per chunk: a vertex (all K_v entries of L_v) or up to kCostRows rows of one
 // edge table W_e[row = later endpoint config][col = earlier endpoint config].  Per-config,
 // per-axis shard extents (and prod need) are precomputed in shared memory, so the inner
-// loop is a min / multiply per axis, and stores are coalesced along the column.
-constexpr int kCostCols = 512;
-
-__global__ void __launch_bounds__(256, 4)
-cost_tables_kernel(const pase_node* __restrict__ nodes, const int32_t* __restrict__ K,
-                   const int64_t* __restrict__ cfg_off, const int32_t* __restrict__ cfg,
-                   const int64_t* __restrict__ loff, int n, const EdgeDesc* __restrict__ edges,
-                   const CostChunk* __restrict__ chunks, double r, double* __restrict__ L,
-                   double* __restrict__ W) {
-    // [axis][config] layouts: lanes of a warp read consecutive configs (conflict-free)
-    __shared__ uint32_t rowq[kMaxDims][kCostRows];
-    __shared__ uint32_t colq[kMaxDims][kCostCols];
-    __shared__ uint64_t rowprod[kCostRows];
-    __shared__ uint64_t colprod[kCostCols];
-    __shared__ pase_node su;                                // the vertex / the edge's producer
-    __shared__ EdgeDesc se;
-    const CostChunk ch = chunks[blockIdx.x];
+// loop is a min / multiply per axis, and stores are coalesced along the column.  Runs as its
+// own kernel (per-vertex launch schedule) or as tasks of the persistent DP kernel.
+__device__ __noinline__ void cost_chunk(const CostArgs& A, int chunk, CostSmem& sm) {
+    const CostChunk ch = A.chunks[chunk];
     // chunk.node = the vertex, or the edge's src: both structs are staged in one round of loads
-    stage_struct(&su, nodes + ch.node);
-    if (ch.item >= n) stage_struct(&se, edges + (ch.item - n));
+    stage_struct(&sm.su, A.nodes + ch.node);
+    if (ch.item >= A.n) stage_struct(&sm.se, A.edges + (ch.item - A.n));
     __syncthreads();
-    if (ch.item < n) {
+    if (ch.item < A.n) {
         const int v = ch.item;
-        const int Kv = K[v];
-        const int32_t* cv = cfg + cfg_off[v] * kMaxDims;
-        double* Lv = L + loff[v];
-        for (int c = threadIdx.x; c < Kv; c += blockDim.x) Lv[c] = d_layer_cost(su, cv + c * kMaxDims, r);
+        const int Kv = A.K[v];
+        const int32_t* cv = A.cfg + A.cfg_off[v] * kMaxDims;
+        double* Lv = A.L + A.loff[v];
+        for (int c = threadIdx.x; c < Kv; c += blockDim.x) Lv[c] = d_layer_cost(sm.su, cv + c * kMaxDims, A.r);
+        __syncthreads();                                    // sm reused by the caller's next chunk
         return;
     }
-    const EdgeDesc& e = se;
-    const pase_node& u = su;
+    const EdgeDesc& e = sm.se;
+    const pase_node& u = sm.su;
     const int nax = u.n_out_axes;
     const int early = e.later_is_src ? e.dst : e.src;
-    const int Ke = K[early];
+    const int Ke = A.K[early];
     const uint64_t elem2 = 2ull * (uint64_t)u.elem_bytes;
     // t_x (DESIGN reading K): per output axis a of src, held_a = ext / c_src, need_a =
     // ceil(ext / c_dst[map_a]) (ext if unmapped); t_x = 2 elem (prod need - prod min(need, held))
     // (sizes < 2^31, validated on the host: 32-bit divisions)
-    const int32_t* cfg_s = cfg + cfg_off[e.src] * kMaxDims;
-    const int32_t* cfg_d = cfg + cfg_off[e.dst] * kMaxDims;
+    const int32_t* cfg_s = A.cfg + A.cfg_off[e.src] * kMaxDims;
+    const int32_t* cfg_d = A.cfg + A.cfg_off[e.dst] * kMaxDims;
     auto held = [&](int cs, int a) -> uint32_t {
         const int32_t* c = cfg_s + cs * kMaxDims;
         return (uint32_t)u.size[u.out_axes[a]] / (uint32_t)c[u.out_axes[a]];
@@ -143,10 +131,10 @@ cost_tables_kernel(const pase_node* __restrict__ nodes, const int32_t* __restric
         uint64_t pr = 1;
         for (int a = 0; a < nax; ++a) {
             const uint32_t x = e.later_is_src ? held(ch.row0 + rr, a) : need(ch.row0 + rr, a);
-            rowq[a][rr] = x;
+            sm.rowq[a][rr] = x;
             pr *= x;
         }
-        rowprod[rr] = pr;
+        sm.rowprod[rr] = pr;
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int c0 = 0; c0 < Ke; c0 += kCostCols) {
@@ -156,30 +144,32 @@ cost_tables_kernel(const pase_node* __restrict__ nodes, const int32_t* __restric
             uint64_t pr = 1;
             for (int a = 0; a < nax; ++a) {
                 const uint32_t x = e.later_is_src ? need(c0 + cc, a) : held(c0 + cc, a);
-                colq[a][cc] = x;
+                sm.colq[a][cc] = x;
                 pr *= x;
             }
-            colprod[cc] = pr;
+            sm.colprod[cc] = pr;
         }
         __syncthreads();
         for (int rr = warp; rr < ch.nrows; rr += nw) {
-            double* out = W + e.woff + (int64_t)(ch.row0 + rr) * Ke + c0;
+            double* out = A.W + e.woff + (int64_t)(ch.row0 + rr) * Ke + c0;
             for (int cc = lane; cc < nc; cc += 32) {
                 uint64_t ov = 1;
-                for (int a = 0; a < nax; ++a) ov *= (uint64_t)min(rowq[a][rr], colq[a][cc]);
-                const uint64_t nd = e.later_is_src ? colprod[cc] : rowprod[rr];
-                out[cc] = __dmul_rn(r, __ull2double_rn((unsigned long long)(elem2 * (nd - ov))));
+                for (int a = 0; a < nax; ++a) ov *= (uint64_t)min(sm.rowq[a][rr], sm.colq[a][cc]);
+                const uint64_t nd = e.later_is_src ? sm.colprod[cc] : sm.rowprod[rr];
+                out[cc] = __dmul_rn(A.r, __ull2double_rn((unsigned long long)(elem2 * (nd - ov))));
             }
         }
     }
+    __syncthreads();                                        // sm reused by the caller's next chunk
 }
 
-void launch_cost_tables(const pase_node* nodes_dev, const int32_t* K_dev, const int64_t* cfg_off_dev,
-                        const int32_t* cfg_dev, const int64_t* loff_dev, int n,
-                        const EdgeDesc* edges_dev, const CostChunk* chunks_dev, int nchunks,
-                        double r, double* L_dev, double* W_dev, void* stream) {
-    cost_tables_kernel<<<(unsigned)nchunks, 256, 0, (cudaStream_t)stream>>>(
-        nodes_dev, K_dev, cfg_off_dev, cfg_dev, loff_dev, n, edges_dev, chunks_dev, r, L_dev, W_dev);
+__global__ void __launch_bounds__(256, 4) cost_tables_kernel(CostArgs A) {
+    __shared__ CostSmem sm;
+    cost_chunk(A, blockIdx.x, sm);
+}
+
+void launch_cost_tables(const CostArgs& A, int nchunks, void* stream) {
+    cost_tables_kernel<<<(unsigned)nchunks, 256, 0, (cudaStream_t)stream>>>(A);
 }
 
 // =====================================================================================
@@ -883,7 +873,7 @@ constexpr uint64_t kSpinTimeoutNs = 4000000000ull;    // a wait this long is rep
 __global__ void __launch_bounds__(256, 2)
 dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ tds,
               const TaskDesc* __restrict__ tasks, const int32_t* __restrict__ order, int ntasks,
-              int32_t* __restrict__ sched, int32_t* __restrict__ err, Peers peers,
+              int32_t* __restrict__ sched, int32_t* __restrict__ err, Peers peers, CostArgs cost,
               int64_t* __restrict__ trace) {
     // sched: [0] claim counter (own 128-B line), [kSchedLine, +n) pending per vertex
     int32_t* head = sched;
@@ -894,6 +884,7 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
     __shared__ double red_b[8 * kTile];                     // latency-mode partial minima
     __shared__ int red_c[8 * kTile];
     __shared__ int s_task;
+    __shared__ CostSmem csm;                                // cost-table tasks
     const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     int cur = -1;
     for (;;) {
@@ -907,6 +898,25 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
         int task = s_task;
         if (task < 0) break;
         const TaskDesc tk = tasks[task];
+        if (tk.vtx < 0) {                                   // cost-table chunk (no dependencies)
+            const int c = -1 - tk.vtx;
+            if (trace && threadIdx.x == 0) t_start = (int64_t)globaltimer();
+            if (cost.enabled) cost_chunk(cost, c, csm);     // ends with a CTA barrier
+            else __syncthreads();
+            if (threadIdx.x == 0) {                         // its consumer's tasks may start
+                int32_t* pc = pending + cost.chunks[c].consumer;
+                if (multi) red_add_release_sys(pc, -1);
+                else atom_add_acq_rel(pc, -1);
+                if (trace) {
+                    int64_t* tr = trace + (int64_t)kTraceWords * task;
+                    tr[0] = ((int64_t)smid() << 32) | (uint32_t)tk.vtx;
+                    tr[1] = t_claim;
+                    tr[2] = t_start;
+                    tr[3] = tr[4] = tr[5] = (int64_t)globaltimer();
+                }
+            }
+            continue;
+        }
         if (tk.vtx != cur) {                                // descriptors: static, fetch now
             if (threadIdx.x == 0) vd = vds[tk.vtx];
             __syncthreads();
@@ -965,10 +975,11 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
 
 void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, const TaskDesc* tasks_dev,
                           const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
-                          const Peers& peers, int nblocks, int64_t* trace_dev, void* stream) {
+                          const Peers& peers, const CostArgs& cost, int nblocks, int64_t* trace_dev,
+                          void* stream) {
     dp_persistent<<<(unsigned)nblocks, 256, 0, (cudaStream_t)stream>>>(vd_dev, td_dev, tasks_dev, order_dev,
                                                                          ntasks, sched_dev, err_dev, peers,
-                                                                         trace_dev);
+                                                                         cost, trace_dev);
 }
 
 // Group barrier between the ranks of a multi-GPU search (before and after the DP): every

@@ -62,10 +62,11 @@ struct EdgeDesc {            // cost-table kernel: one per edge
     int64_t woff;            // doubles
 };
 
-struct CostChunk {           // cost-table kernel work unit (one CTA)
+struct CostChunk {           // cost-table work unit (one CTA)
     int32_t item;            // < n: vertex (all of L_v); >= n: edge item - n
     int32_t row0, nrows;     // edge: rows [row0, row0 + nrows) of W_e (later-endpoint configs)
     int32_t node;            // the vertex, or the edge's src (staged with the edge descriptor)
+    int32_t consumer;        // rank of the DP vertex that reads it (persistent schedule)
 };
 
 struct TermDesc {            // one summand of Eq. 4 for a vertex (L, one W_e, or one child T_j)
@@ -141,8 +142,12 @@ struct SchedPlan {           // build_schedule output for one rank
 
 // schedule.cpp: tasks, broadcast flags, pending counters and claim order (needs VertexDesc
 // shape / tiling / part fields filled in).
+// chunk_consumer (optional): per cost-table chunk the rank of the DP vertex reading it; the
+// chunks then become tasks of the persistent schedule (vtx = -1 - chunk) that the consumer's
+// tasks wait for.
 pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world, int rank, int nblocks,
-                           SchedPlan& out, std::string& err);
+                           SchedPlan& out, std::string& err,
+                           const std::vector<int32_t>* chunk_consumer = nullptr);
 constexpr int kTile = 8;     // max outputs per lane group along qstar
 constexpr int kTile1 = 4, kTile2 = 4;   // 2-D tile: outputs along qstar x q2
 constexpr int kShape2D = 64;            // shapes >= kShape2D: 2-D tiled (NS-1)*4 + (glog-2)
@@ -150,6 +155,30 @@ constexpr int kShape2S = 96;            // shapes >= kShape2S: 2-D single-suffix
 //   form 0: P1 = [A], S = [S1]; 1: P1 = [A, B], S = [S1]; 2: S = [S1, const]; 3: S = [S1, S2 on q1]
 constexpr int kMaxP0 = 4, kMaxP1 = 2;   // 2-D tile: max scalar-prefix / q2-prefix terms
 constexpr int kCostRows = 64;  // edge-table rows per cost-table CTA
+constexpr int kCostCols = 512; // edge-table columns staged per pass
+
+struct CostArgs {            // the cost-table computation (kernel parameter)
+    const pase_node* nodes;
+    const int32_t* K;
+    const int64_t* cfg_off;
+    const int32_t* cfg;
+    const int64_t* loff;
+    int32_t n, enabled;      // enabled = 0: tables were given by pase_set_cost_tables
+    const EdgeDesc* edges;
+    const CostChunk* chunks;
+    double r;
+    double* L;
+    double* W;
+};
+
+struct CostSmem {            // its shared memory ([axis][config]: conflict-free over configs)
+    uint32_t rowq[kMaxDims][kCostRows];
+    uint32_t colq[kMaxDims][kCostCols];
+    uint64_t rowprod[kCostRows];
+    uint64_t colprod[kCostCols];
+    pase_node su;            // the vertex / the edge's producer
+    EdgeDesc se;
+};
 
 struct BtDesc {               // back-substitution record of one rank, in back-level order
     const uint16_t* A;       // argmin table A(i)
@@ -167,15 +196,13 @@ struct EvalEdge {             // Eq. 1 kernels (eval.cu): W_e element = W[off + 
 constexpr int kBruteThreads = 128;
 
 // kernels.cu entry points (host-side launchers)
-void launch_cost_tables(const pase_node* nodes_dev, const int32_t* K_dev, const int64_t* cfg_off_dev,
-                        const int32_t* cfg_dev, const int64_t* loff_dev, int n,
-                        const EdgeDesc* edges_dev, const CostChunk* chunks_dev, int nchunks,
-                        double r, double* L_dev, double* W_dev, void* stream);
+void launch_cost_tables(const CostArgs& A, int nchunks, void* stream);
 void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vertex,
                       const VertexDesc& vd_host, void* stream);
 void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, const TaskDesc* tasks_dev,
                           const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
-                          const Peers& peers, int nblocks, int64_t* trace_dev, void* stream);
+                          const Peers& peers, const CostArgs& cost, int nblocks, int64_t* trace_dev,
+                          void* stream);
 void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev, void* stream);
 int persistent_blocks_per_sm();
 void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,

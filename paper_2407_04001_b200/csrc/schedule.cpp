@@ -30,7 +30,7 @@ namespace pase {
 static const bool kWaveTail = !(std::getenv("PASE_WAVE_TAIL") && std::getenv("PASE_WAVE_TAIL")[0] == '0');
 
 pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world, int rank, int nblocks,
-                           SchedPlan& out, std::string& err) {
+                           SchedPlan& out, std::string& err, const std::vector<int32_t>* chunk_consumer) {
     const int n = P.n;
     const int G = std::max(world, 1);
     nblocks = std::max(nblocks, 1);
@@ -39,7 +39,10 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     // ---- per (vertex, rank): unit runs, split into tasks
     struct GTask { int32_t rank, vtx; int64_t i0, i1; int32_t glog; };   // glog 0 = the vertex's
     std::vector<GTask> all;
-    std::vector<std::vector<std::vector<int32_t>>> tasks_of(n, std::vector<std::vector<int32_t>>(G));
+    // tasks_of[i] for DP vertex i; tasks_of[n + i] = the cost-table chunks vertex i reads (run by
+    // every rank: each needs the full L / W tables), which its tasks wait for like children
+    const int nv = chunk_consumer ? 2 * n : n;
+    std::vector<std::vector<std::vector<int32_t>>> tasks_of(nv, std::vector<std::vector<int32_t>>(G));
     for (int i = 0; i < n; ++i) {
         const VertexDesc& d = vd[i];
         const int64_t units = d.shape >= 0 ? d.nitems : d.nout;
@@ -92,6 +95,12 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
                 }
         }
     }
+    if (chunk_consumer)
+        for (int c = 0; c < (int)chunk_consumer->size(); ++c)
+            for (int q = 0; q < G; ++q) {
+                tasks_of[n + (*chunk_consumer)[c]][q].push_back((int32_t)all.size());
+                all.push_back({q, n + (*chunk_consumer)[c], c, c + 1, 0});
+            }
     // ---- broadcast flags (bit 0: T, bit 1: A)
     for (int j = 0; j < n; ++j) {
         VertexDesc& d = vd[j];
@@ -118,7 +127,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     };
     std::vector<std::vector<int64_t>> pend(G, std::vector<int64_t>(n));
     for (int q = 0; q < G; ++q)
-        for (int p = 0; p < n; ++p) pend[q][p] = waits_on(p, q);
+        for (int p = 0; p < n; ++p) pend[q][p] = waits_on(p, q) + (nv > n ? (int64_t)tasks_of[n + p][q].size() : 0);
     out.pending.assign(n, 0);
     for (int p = 0; p < n; ++p) {
         if (pend[rank][p] > INT32_MAX) { err = "internal: pending counter overflow"; return PASE_ERR_RESOURCE; }
@@ -127,8 +136,9 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     // ---- global list schedule: per-rank pools of nblocks CTAs, critical path first.
     // Estimated task time: ~3 us dependent-latency overhead + candidates at ~3e9/s per CTA.
     const int64_t ntk = (int64_t)all.size();
-    std::vector<double> tdur(ntk), bl(n, 0.0);
+    std::vector<double> tdur(ntk), bl(nv, 0.0);
     for (int64_t t = 0; t < ntk; ++t) {
+        if (all[t].vtx >= n) { tdur[t] = 4.0; continue; }  // a cost-table chunk
         const VertexDesc& d = vd[all[t].vtx];
         const double cand = (double)(all[t].i1 - all[t].i0) * d.K * (d.shape < 0 ? 1 : d.q2 >= 0 ? kTile1 * kTile2 : kTile);
         const double lanes = all[t].glog ? (double)(1 << (all[t].glog - d.glog)) : 1.0;   // wave tail
@@ -141,6 +151,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         const double vt = std::max(longest, work / ((double)nblocks * G));
         bl[i] = vt + (P.parent[i] >= 0 ? bl[P.parent[i]] : 0.0);
     }
+    for (int i = n; i < nv; ++i) bl[i] = 4.0 + bl[i - n];
     const auto tt1 = std::chrono::steady_clock::now();
     std::vector<double> start(ntk, -1.0);
     {
@@ -148,16 +159,16 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         // one entry per released run and a cursor walks the run's tasks
         using RT = std::pair<double, int32_t>;                         // (priority, -(v*G+q))
         std::vector<std::priority_queue<RT>> ready(G);
-        std::vector<int32_t> cursor((size_t)n * G, 0);
+        std::vector<int32_t> cursor((size_t)nv * G, 0);
         // an event finishes k equal-length tasks of one run started at the same time
         struct EV { double t; int32_t vq, k; bool operator>(const EV& o) const { return t != o.t ? t > o.t : vq > o.vq; } };
         std::priority_queue<EV, std::vector<EV>, std::greater<EV>> events;
         auto release = [&](int v, int q) {
             if (!tasks_of[v][q].empty()) ready[q].push({bl[v], -(v * G + q)});
         };
-        for (int i = 0; i < n; ++i)
-            if (P.children[i].empty())
-                for (int q = 0; q < G; ++q) release(i, q);
+        for (int i = 0; i < nv; ++i)
+            for (int q = 0; q < G; ++q)
+                if (i >= n || pend[q][i] == 0) release(i, q);
         std::vector<int> free_w(G, nblocks);
         double now = 0.0;
         int64_t started = 0;
@@ -184,6 +195,10 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
             now = e.t;
             const int v = e.vq / G, q0 = e.vq % G;
             free_w[q0] += e.k;
+            if (v >= n) {                               // cost chunks of vertex v - n done
+                if ((pend[q0][v - n] -= e.k) == 0) release(v - n, q0);
+                continue;
+            }
             const int par = P.parent[v];
             if (par < 0) continue;
             if (vd[v].bcast & 1) {
@@ -215,6 +230,11 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         }
         vd[i].ntasks = (int32_t)tasks_of[i][rank].size();
     }
+    for (int i = n; i < nv; ++i)                        // cost-table tasks: vtx = -1 - chunk
+        for (int32_t t : tasks_of[i][rank]) {
+            local_id[t] = (int32_t)out.tasks.size();
+            out.tasks.push_back({(int32_t)(-1 - all[t].i0), 0, 0, 0});
+        }
     for (int32_t t : mine) out.order.push_back(local_id[t]);
     out.total_tasks = ntk;
     return PASE_OK;

@@ -49,6 +49,11 @@ def _worker(rank, world, port, q):
         q.put(("err", repr(e)))
 
 
+def zoo_graph(name):
+    from paper_2407_04001_b200 import zoo
+    return zoo.bench_graph(name)
+
+
 def _units(K, deps_i):
     n = 1
     for u in deps_i:
@@ -103,11 +108,23 @@ def test_two_rank_partition_plan(world):
                 top = r0["deps"][i][-1]
                 aligned = par >= 0 and bool(r0["vinfo"][par, 0]) and r0["deps"][par][-1] in r0["deps"][i]
                 assert bool(bcast & 1) == (not aligned)
-        # pending counters: children's tasks each rank waits for
+        # pending counters: children's tasks each rank waits for (plus, with PASE_COST_TASKS=1, the cost-table chunks
+        # the vertex reads (its L, and W of the edges it pays: 64-row chunks of the later
+        # endpoint's configs), which every rank computes itself
+        g, _ = zoo_graph(name)
+        rank_of = {int(v): i for i, v in enumerate(r0["sigma"])}
+        chunks_of = [1] * n
+        for ed in g["edges"]:
+            a, b = rank_of[ed["src"]], rank_of[ed["dst"]]
+            late = ed["src"] if a > b else ed["dst"]
+            chunks_of[min(a, b)] += -(-int(r0["K"][late]) // 64)
+        if os.environ.get("PASE_COST_TASKS") != "1":
+            chunks_of = [0] * n
         for rk, r in enumerate(ranks):
+            assert int((r["tasks"][:, 0] < 0).sum()) == sum(chunks_of)
             for p_ in range(n):
                 kids = [j for j in range(n) if int(r0["parent"][j]) == p_]
-                want = 0
+                want = chunks_of[p_]
                 for j in kids:
                     if int(r0["vinfo"][j, 1]) & 1:
                         want += sum(int(x["vinfo"][j, 2]) for x in ranks)
