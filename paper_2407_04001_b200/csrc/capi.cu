@@ -239,6 +239,58 @@ bool no_2d() {
 // multi-GPU partition coordinate) whose first term is latest; use the 2-D tile when its
 // segment structure fits the kernel and it cuts the loads per candidate by >= 20 % on a
 // vertex whose 1-D form is load-heavy.
+// Lane-group widening on the critical path.  Estimated vertex time = waves of
+// one-round tasks x (3 us + candidates per task / 6000 per us); a vertex whose longest
+// leaf-to-root path through it is >= 85 % of the longest is critical (re-evaluated after each
+// round of widening).  A critical vertex whose
+// one-round tasks do not fill the grid widens its lane groups (every tile family
+// encodes log2 G in the shape's low 2 bits; >= 8 values of C per lane kept) until they do:
+// its K/G serial iterations -- the latency on the chain -- shrink, and the idle CTAs take the
+// extra tasks.  Non-critical vertices keep the efficient narrow groups (widening every
+// few-task vertex was measured slower, profiles/r01_ab_scheduling.txt).
+void widen_critical(pase_ctx* ctx) {
+    static const bool widen = !(std::getenv("PASE_WIDEN") && std::getenv("PASE_WIDEN")[0] == '0');
+    if (!widen) return;
+    const Plan& P = ctx->P;
+    const int n = P.n;
+    const int64_t nb = ctx->nblocks;
+    auto tasks_of = [&](const VertexDesc& d) -> int64_t {
+        const int64_t items = std::max<int64_t>(1, d.nitems / (d.part ? ctx->world : 1));
+        return std::max<int64_t>(1, ((items << d.glog) + 255) / 256);
+    };
+    // (rates from PASE_TRACE timelines: ~6000 candidates per us per CTA for the tiled
+    // shapes; one-round latency-mode / generic tasks ~5.5 us)
+    auto est = [&](const VertexDesc& d) -> double {
+        const double cand = (double)d.nout * d.K / (d.part ? ctx->world : 1);
+        if (d.shape < 0 || d.wlog > 0) return 5.5 + cand / 6000.0 / (double)nb;
+        const int64_t T = tasks_of(d);
+        return (double)((T + nb - 1) / nb) * (3.0 + cand / (double)T / 6000.0);
+    };
+    // a few rounds: widening the critical chain can make another chain critical
+    for (int round = 0; round < 4; ++round) {
+        std::vector<double> w(n), top(n), bot(n);
+        for (int i = 0; i < n; ++i) w[i] = est(ctx->vd[i]) + 1.0;      // + dependency latency
+        for (int i = 0; i < n; ++i) {                                  // children: lower ranks
+            double mx = 0.0;
+            for (int j : P.children[i]) mx = std::max(mx, top[j]);
+            top[i] = w[i] + mx;
+        }
+        for (int i = n - 1; i >= 0; --i) bot[i] = w[i] + (P.parent[i] >= 0 ? bot[P.parent[i]] : 0.0);
+        const double cp = top[n - 1];
+        bool changed = false;
+        for (int i = 0; i < n; ++i) {
+            VertexDesc& d = ctx->vd[i];
+            if (top[i] + bot[i] - w[i] < 0.85 * cp || d.shape < 0 || d.wlog != 0) continue;
+            while (d.glog < 5 && (16 << d.glog) <= d.K && tasks_of(d) < nb) {
+                ++d.glog;
+                d.shape = (d.shape & ~3) | (d.glog - 2);
+                changed = true;
+            }
+        }
+        if (!changed) break;
+    }
+}
+
 // single-suffix 2-D tile only for vertices with at least this many candidates
 const int64_t kMin2S = std::getenv("PASE_MIN_2S") ? std::atoll(std::getenv("PASE_MIN_2S")) : (int64_t(1) << 24);
 
@@ -427,22 +479,6 @@ pase_status prepare(pase_ctx* ctx, bool device) {
 
     ctx->vd.assign(n, VertexDesc{});
     ctx->td.clear();
-    // critical vertices (by candidates): the longest candidate-weighted path from a leaf to the
-    // root through i is >= 90 % of the longest overall.  Only those widen their lane groups
-    // below (a vertex running beside many others widened loses throughput for nothing)
-    std::vector<char> critical(n, 0);
-    {
-        std::vector<double> w(n), top(n), bot(n);
-        for (int i = 0; i < n; ++i) w[i] = (double)P.tsize[i] * (double)P.K[P.sigma[i]];
-        for (int i = 0; i < n; ++i) {                       // children have lower ranks
-            double mx = 0.0;
-            for (int j : P.children[i]) mx = std::max(mx, top[j]);
-            top[i] = w[i] + mx;
-        }
-        for (int i = n - 1; i >= 0; --i) bot[i] = w[i] + (P.parent[i] >= 0 ? bot[P.parent[i]] : 0.0);
-        const double cp = top[n - 1];
-        for (int i = 0; i < n; ++i) critical[i] = top[i] + bot[i] - w[i] >= 0.9 * cp;
-    }
     for (int i = 0; i < n; ++i) {
         const int v = P.sigma[i];
         VertexDesc& d = ctx->vd[i];
@@ -540,24 +576,12 @@ pase_status prepare(pase_ctx* ctx, bool device) {
             }
             d.shape = (NP - 1) * 16 + NS * 4 + (d.glog - 2);
             if (d.wlog == 0 && !no_2d()) try_tile2(ctx, d, tv, top);
-            // a big vertex whose one-round tasks would not fill the grid widens its lane groups
-            // (all tile families encode log2 G in the shape's low 2 bits) until they do: its
-            // tasks then run K/G serial iterations in parallel on every CTA instead of twice as
-            // many on half of them
-            static const bool widen = !(std::getenv("PASE_WIDEN") && std::getenv("PASE_WIDEN")[0] == '0');
-            if (widen && critical[i] && d.shape >= 0 && d.wlog == 0 && d.nout * d.K >= kMin2S) {
-                const int64_t items = std::max<int64_t>(1, d.nitems / (d.part ? ctx->world : 1));
-                while (d.glog < 5 && (16 << d.glog) <= d.K &&
-                       (items * (int64_t(1) << d.glog) + 255) / 256 < ctx->nblocks) {
-                    ++d.glog;
-                    d.shape = (d.shape & ~3) | (d.glog - 2);
-                }
-            }
         } else {                                          // generic kernel
             d.glog = d.K <= 4 ? 2 : d.K <= 8 ? 3 : d.K <= 16 ? 4 : 5;
             d.shape = -1;
         }
     }
+    widen_critical(ctx);
     // tasks, broadcast flags, pending counters, claim order (schedule.cpp)
     std::vector<int32_t> consumer(chunks.size());
     for (size_t k = 0; k < chunks.size(); ++k) consumer[k] = chunks[k].consumer;
