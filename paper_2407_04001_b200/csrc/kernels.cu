@@ -17,6 +17,17 @@
 #define PASE_CUNROLL 2   // C iterations in flight per lane in the 1-D tile loop
 #endif
 constexpr int kCUnroll = PASE_CUNROLL;
+// persistent-scheduler synchronisation variants (A/B builds; defaults = measured best,
+// profiles/r01_ab_scheduling.txt: the fence + spin pair is 2-9 % faster on every workload)
+#ifndef PASE_SPIN_SLEEP
+#define PASE_SPIN_SLEEP 0      // back off with __nanosleep while polling a pending counter
+#endif
+#ifndef PASE_ACQ_FENCE
+#define PASE_ACQ_FENCE 1       // acquire via fence.acq_rel after the relaxed poll (else ld.acquire)
+#endif
+#ifndef PASE_REL_RED
+#define PASE_REL_RED 0         // release via red.release (no return) instead of atom.acq_rel
+#endif
 
 namespace pase {
 
@@ -855,6 +866,10 @@ __device__ __forceinline__ int atom_add_acq_rel(int32_t* p, int v) {
     return old;
 }
 
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_add_release_gpu(int32_t* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ int ld_acquire_sys(const int32_t* p) {
     int v;
     asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -930,12 +945,15 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
                 unsigned bo = 32;
                 const uint64_t t0 = globaltimer();
                 while ((multi ? ld_relaxed_sys(pv) : ld_relaxed(pv)) != 0) {
-                    __nanosleep(bo);
-                    bo = bo < 256 ? 2 * bo : 256;
+                    if (PASE_SPIN_SLEEP) {
+                        __nanosleep(bo);
+                        bo = bo < 256 ? 2 * bo : 256;
+                    }
                     if (globaltimer() - t0 > kSpinTimeoutNs) { atomicExch(err, 1); s_task = -1; break; }
                 }
             }
             if (multi) (void)ld_acquire_sys(pv);
+            else if (PASE_ACQ_FENCE) fence_acquire_gpu();      // relaxed read + fence = acquire pattern
             else (void)ld_acquire(pv);
             if (trace) t_start = (int64_t)globaltimer();
         }
@@ -956,6 +974,8 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
                     for (int q = 0; q < peers.world; ++q) red_add_release_sys(peers.pending[q] + vd.parent, -1);
                 } else if (multi) {
                     red_add_release_sys(pending + vd.parent, -1);
+                } else if (PASE_REL_RED) {
+                    red_add_release_gpu(pending + vd.parent, -1);
                 } else {
                     atom_add_acq_rel(pending + vd.parent, -1);
                 }
