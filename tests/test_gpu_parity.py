@@ -91,6 +91,13 @@ def test_transformer_le_p():
     run_pair(g, p, "le_p", tables=False)
 
 
+def test_gnmt_le_p():
+    """The single-suffix 2-D tile forms with a trailing prefix / suffix term are
+    what GNMT LE_P's big vertices use."""
+    g, p = zoo.bench_graph("gnmt")
+    run_pair(g, p, "le_p", tables=False)
+
+
 @pytest.mark.parametrize("kind", ["int", "real"])
 def test_random_synthetic_costs(kind):
     """Theorem-1-style random graphs with explicit costs: ties (int) and rounding (real)."""

@@ -1,0 +1,32 @@
+"""Every tuning switch of DESIGN §6.1 keeps the results bit-exact: the parity checks of
+tests/test_gpu_parity.py re-run in a subprocess per switch setting (the switches are read once
+per process).  Forcing the single-suffix 2-D forms, the wave tail and the widening onto small
+graphs exercises code paths the default plans reserve for the big zoo vertices."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+VARIANTS = {
+    "2s_everywhere": {"PASE_MIN_2S": "0"},
+    "no_2d": {"PASE_NO_2D": "1"},
+    "no_latency_mode": {"PASE_LATENCY_CAND": "0"},
+    "narrow_groups": {"PASE_C_PER_LANE": "8"},
+    "no_tail_no_widen": {"PASE_WAVE_TAIL": "0", "PASE_WIDEN": "0"},
+    "cost_tasks": {"PASE_COST_TASKS": "1"},
+}
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+def test_switch_keeps_parity(variant):
+    env = dict(os.environ)
+    env.update(VARIANTS[variant])
+    env["PYTHONPATH"] = ROOT + os.pathsep + env.get("PYTHONPATH", "")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "parity_variant_main.py"),
+                        "mlp,alexnet,inception_v3,transformer", "12"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "variant parity ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
