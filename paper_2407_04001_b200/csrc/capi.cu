@@ -582,6 +582,8 @@ pase_status prepare(pase_ctx* ctx, bool device) {
         }
     }
     widen_critical(ctx);
+    for (VertexDesc& d : ctx->vd)                         // partitioned item order (split_item)
+        d.psub = (d.part && d.shape >= 0) ? (int32_t)(d.ncombo / d.radix[d.m - 1]) : 1;
     // tasks, broadcast flags, pending counters, claim order (schedule.cpp)
     std::vector<int32_t> consumer(chunks.size());
     for (size_t k = 0; k < chunks.size(); ++k) consumer[k] = chunks[k].consumer;

@@ -201,6 +201,21 @@ __device__ __forceinline__ void combine(double& b, int& c, double ob, int oc) {
     if (ob < b || (ob == b && oc < c)) { b = ob; c = oc; }
 }
 
+// Item -> (combination of the untiled coordinates, tile index).  Single GPU: combinations
+// fastest (the warps of a CTA share a tile: L1 reuse).  Multi-GPU partitioned vertex (vd.part):
+// [combinations below the partition coordinate] fastest, then the tile, then the partition
+// coordinate -- so each rank's share of the vertex is ONE contiguous item range.
+__device__ __forceinline__ void split_item(const VertexDesc& vd, uint32_t it, uint32_t& combo, uint32_t& tile) {
+    if (vd.part) {
+        const uint32_t S = (uint32_t)vd.psub, low = it % S, t2 = it / S;
+        tile = t2 % (uint32_t)vd.ntile;
+        combo = low + S * (t2 / (uint32_t)vd.ntile);
+    } else {
+        combo = it % (uint32_t)vd.ncombo;
+        tile = it / (uint32_t)vd.ncombo;
+    }
+}
+
 template <int N>
 struct Log2 { static constexpr int value = 1 + Log2<N / 2>::value; };
 template <>
@@ -269,8 +284,10 @@ __device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td
         const bool valid = item < end;
         const uint32_t it = valid ? (uint32_t)item : 0u;   // host guarantees nitems < 2^31
         const uint32_t nc = (uint32_t)vd.ncombo;
-        uint32_t rem = it % nc;                             // combos fastest: warps of a CTA
-        const int x0 = (int)(it / nc) * V;                  // share the qstar tile (L1 reuse)
+        uint32_t rem, tix;                                  // combos fastest: warps of a CTA
+        split_item(vd, it, rem, tix);                       // share the qstar tile (L1 reuse)
+        (void)nc;
+        const int x0 = (int)tix * V;
         const int nb = valid ? min(V, vd.rq - x0) : 0;
         const double* pp[NP];
         const double* sp[NS > 0 ? NS : 1];
@@ -404,8 +421,9 @@ __device__ __noinline__ void tile2_items(const VertexDesc& vd, const TermDesc* t
         const bool valid = item < end;
         const uint32_t it = valid ? (uint32_t)item : 0u;
         const uint32_t nc = (uint32_t)vd.ncombo;
-        uint32_t rem = it % nc;
-        const uint32_t tidx = it / nc;
+        uint32_t rem, tidx;
+        split_item(vd, it, rem, tidx);
+        (void)nc;
         const int x2 = (int)(tidx % (uint32_t)vd.ntile2) * V2;
         const int x1 = (int)(tidx / (uint32_t)vd.ntile2) * V1;
         const int nb1 = valid ? min(V1, vd.rq - x1) : 0;
@@ -567,8 +585,9 @@ __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* 
         const bool valid = item < end;
         const uint32_t it = valid ? (uint32_t)item : 0u;
         const uint32_t nc = (uint32_t)vd.ncombo;
-        uint32_t rem = it % nc;
-        const uint32_t tidx = it / nc;
+        uint32_t rem, tidx;
+        split_item(vd, it, rem, tidx);
+        (void)nc;
         const int x2 = (int)(tidx % (uint32_t)vd.ntile2) * V2;
         const int x1 = (int)(tidx / (uint32_t)vd.ntile2) * V1;
         const int nb1 = valid ? min(V1, vd.rq - x1) : 0;

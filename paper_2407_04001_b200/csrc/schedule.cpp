@@ -55,10 +55,9 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
                 const int top = d.m - 1;
                 const int64_t Kt = d.radix[top];
                 const int64_t lo = q * Kt / G, hi = (q + 1) * Kt / G;
-                if (d.shape >= 0) {              // items = combo + ncombo * tile; top is combo's slowest
+                if (d.shape >= 0) {              // items: [low combos] fastest, tile, top (split_item)
                     const int64_t S = d.ncombo / Kt;
-                    for (int64_t xt = 0; xt < d.ntile; ++xt)
-                        if (hi > lo) runs.push_back({xt * d.ncombo + lo * S, xt * d.ncombo + hi * S});
+                    if (hi > lo) runs.push_back({lo * S * d.ntile, hi * S * d.ntile});
                 } else {                         // items = outputs; top is the slowest coordinate
                     const int64_t S = d.nout / Kt;
                     if (hi > lo) runs.push_back({lo * S, hi * S});
