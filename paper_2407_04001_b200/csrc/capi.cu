@@ -83,6 +83,7 @@ struct pase_ctx {
     pase::SchedPlan sp;
     int32_t* h_choice = nullptr;            // pinned
     double* h_total = nullptr;              // pinned
+    void* h_total_dev = nullptr;            // its device-mapped address (nullptr: copy instead)
     int32_t* h_err = nullptr;               // pinned
     bool override_tables = false;
     bool solved = false;
@@ -731,9 +732,12 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
             }
     }
     CUDA_TRY(cudaEventRecordWithFlags(ctx->ev_dp, s, ext));
+    // the back-substitution kernel stores the result block straight into the pinned host block
+    // (device-mapped); without a mapping, one D2H copy of it
     pase::launch_backtrack(ctx->d_bt, ctx->d_bt_off, ctx->nbtlev, n, ctx->vd[n - 1].T, ctx->d_choice,
-                           ctx->d_total, s);
-    CUDA_TRY(cudaMemcpyAsync(ctx->h_total, ctx->d_total, 16 + sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+                           ctx->d_total, ctx->d_err, ctx->h_total_dev, s);
+    if (!ctx->h_total_dev)
+        CUDA_TRY(cudaMemcpyAsync(ctx->h_total, ctx->d_total, 16 + sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
     cudaError_t ce = cudaSuccess;
     cudaGraph_t graph = nullptr;
     if (capture) ce = cudaStreamEndCapture(s, &graph);
@@ -888,6 +892,11 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
         ctx->h_total = (double*)h;
         ctx->h_err = (int32_t*)((char*)h + 8);
         ctx->h_choice = (int32_t*)((char*)h + 16);
+        const char* mo = std::getenv("PASE_MAPPED_OUT");
+        if ((mo && mo[0] == '0') || cudaHostGetDevicePointer(&ctx->h_total_dev, h, 0) != cudaSuccess) {
+            ctx->h_total_dev = nullptr;
+            cudaGetLastError();
+        }
     }
     if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
         cudaEventCreate(&ctx->ev_mid) != cudaSuccess || cudaEventCreate(&ctx->ev_dp) != cudaSuccess) {

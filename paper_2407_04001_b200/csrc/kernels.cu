@@ -1053,24 +1053,27 @@ int persistent_blocks_per_sm() {
 // levels, a thread per vertex, choices in shared memory.
 // =====================================================================================
 template <bool SMEM>
-__global__ void __launch_bounds__(1024)
-backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt_off, int nlev, int n,
-                 const double* __restrict__ root_T, int32_t* __restrict__ choice, double* __restrict__ total) {
+__global__ void __launch_bounds__(256)
+backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt_off_g, int nlev, int n,
+                 const double* __restrict__ root_T, int32_t* __restrict__ choice, double* __restrict__ total,
+                 const int32_t* __restrict__ err, char* __restrict__ host_out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    // SMEM: records staged once (coalesced), choices kept on chip; only the A(i) reads of
-    // the dependent chain go to memory (L2-resident: the DP has just written them).
+    // SMEM: records and level offsets staged once (coalesced), choices kept on chip; only the
+    // A(i) reads of the dependent chain go to memory (L2-resident: the DP has just written them)
     BtDesc* sh_bt = reinterpret_cast<BtDesc*>(smem_raw);
     int32_t* sh_choice = reinterpret_cast<int32_t*>(smem_raw + sizeof(BtDesc) * (size_t)n);
+    int32_t* sh_off = sh_choice + n;
     const BtDesc* bt = SMEM ? sh_bt : bt_g;
     int32_t* ch = SMEM ? sh_choice : choice;
+    const int32_t* bt_off = SMEM ? sh_off : bt_off_g;
     if (SMEM) {
         const int words = (int)(sizeof(BtDesc) / 4) * n;
         const int32_t* src = reinterpret_cast<const int32_t*>(bt_g);
         int32_t* dst = reinterpret_cast<int32_t*>(sh_bt);
         for (int k = threadIdx.x; k < words; k += blockDim.x) dst[k] = src[k];
+        for (int k = threadIdx.x; k <= nlev; k += blockDim.x) sh_off[k] = bt_off_g[k];
         __syncthreads();
     }
-    if (threadIdx.x == 0) *total = root_T[0];             // f(|V|, ∅)
     for (int lev = 0; lev < nlev; ++lev) {
         for (int k = bt_off[lev] + threadIdx.x; k < bt_off[lev + 1]; k += blockDim.x) {
             const BtDesc& d = bt[k];
@@ -1083,19 +1086,34 @@ backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt
         }
         __syncthreads();
     }
-    if (SMEM)
-        for (int v = threadIdx.x; v < n; v += blockDim.x) choice[v] = sh_choice[v];
+    // results: the device block (total | err | pad | choice[n]) and, when given, the same
+    // layout straight into the caller's pinned host block (mapped: no copy-engine round trip)
+    int32_t* hc = host_out ? reinterpret_cast<int32_t*>(host_out + 16) : nullptr;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) {
+        const int32_t c = ch[v];
+        if (SMEM) choice[v] = c;
+        if (hc) hc[v] = c;
+    }
+    if (threadIdx.x == 0) {
+        const double t = root_T[0];                         // f(|V|, ∅)
+        *total = t;
+        if (host_out) {
+            *reinterpret_cast<double*>(host_out) = t;
+            *reinterpret_cast<int32_t*>(host_out + 8) = *err;
+        }
+    }
 }
 
 void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,
-                      const double* root_T, int32_t* choice_dev, double* total_dev, void* stream) {
-    const size_t smem = (sizeof(BtDesc) + sizeof(int32_t)) * (size_t)n;
+                      const double* root_T, int32_t* choice_dev, double* total_dev, const int32_t* err_dev,
+                      void* host_out, void* stream) {
+    const size_t smem = (sizeof(BtDesc) + sizeof(int32_t)) * (size_t)n + sizeof(int32_t) * (size_t)(nlev + 1);
     if (smem <= 48 * 1024)
-        backtrack_kernel<true><<<1, 1024, smem, (cudaStream_t)stream>>>(bt_dev, bt_off_dev, nlev, n, root_T,
-                                                                       choice_dev, total_dev);
+        backtrack_kernel<true><<<1, 256, smem, (cudaStream_t)stream>>>(bt_dev, bt_off_dev, nlev, n, root_T,
+                                                                      choice_dev, total_dev, err_dev, (char*)host_out);
     else
-        backtrack_kernel<false><<<1, 1024, 0, (cudaStream_t)stream>>>(bt_dev, bt_off_dev, nlev, n, root_T,
-                                                                     choice_dev, total_dev);
+        backtrack_kernel<false><<<1, 256, 0, (cudaStream_t)stream>>>(bt_dev, bt_off_dev, nlev, n, root_T,
+                                                                    choice_dev, total_dev, err_dev, (char*)host_out);
 }
 
 }  // namespace pase

@@ -207,7 +207,8 @@ void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, cons
 void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev, void* stream);
 int persistent_blocks_per_sm();
 void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,
-                      const double* root_T, int32_t* choice_dev, double* total_dev, void* stream);
+                      const double* root_T, int32_t* choice_dev, double* total_dev, const int32_t* err_dev,
+                      void* host_out, void* stream);
 
 // assign.cpp (row f3): greedy device assignment of a strategy (DESIGN reading U)
 pase_status assign_devices(const Plan& P, const int32_t* config_index, int32_t* device_out, double* tx_out,
