@@ -698,15 +698,27 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
     if (capture) CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     const unsigned ext = capture ? cudaEventRecordExternal : cudaEventRecordDefault;
     int32_t* d_err = ctx->d_err;
-    CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int32_t), s));
-    // cost tables: tasks of the persistent kernel (the DP's first tasks overlap them); the
-    // per-vertex launch schedule runs them as their own kernel first
-    if (!ctx->override_tables && !ctx->cost_tasks) pase::launch_cost_tables(cost_args(ctx), ctx->nchunks, s);
+    // the cost-table kernel also resets the error flag and the persistent scheduler's state
+    // (claim counter, pending counters) before the DP kernel starts: no memset / copy nodes
+    const bool fold = !ctx->override_tables && !ctx->cost_tasks;
+    if (fold) {
+        pase::CostArgs ca = cost_args(ctx);
+        ca.err = d_err;
+        if (ctx->persistent) {
+            ca.sched = ctx->d_sched;
+            ca.sched_init = ctx->d_sched_init;
+            ca.sched_words = (int32_t)(ctx->sched_bytes / sizeof(int32_t));
+        }
+        pase::launch_cost_tables(ca, ctx->nchunks, s);
+    } else {
+        CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int32_t), s));
+    }
     // phase split: external event nodes (plain records would only become capture edges)
     CUDA_TRY(cudaEventRecordWithFlags(ctx->ev_mid, s, ext));
     std::vector<char> used(nstreams, 0);
     if (ctx->persistent) {
-        CUDA_TRY(cudaMemcpyAsync(ctx->d_sched, ctx->d_sched_init, ctx->sched_bytes, cudaMemcpyDeviceToDevice, s));
+        if (!fold)
+            CUDA_TRY(cudaMemcpyAsync(ctx->d_sched, ctx->d_sched_init, ctx->sched_bytes, cudaMemcpyDeviceToDevice, s));
         if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, s);
         pase::launch_dp_persistent(ctx->d_vd, ctx->d_td, ctx->d_tasks, ctx->d_order, ctx->ntasks, ctx->d_sched,
                                    d_err, ctx->peers, cost_args(ctx), ctx->nblocks,

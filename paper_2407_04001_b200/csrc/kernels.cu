@@ -176,6 +176,11 @@ __device__ __noinline__ void cost_chunk(const CostArgs& A, int chunk, CostSmem& 
 
 __global__ void __launch_bounds__(256, 4) cost_tables_kernel(CostArgs A) {
     __shared__ CostSmem sm;
+    if (blockIdx.x == 0) {                                  // per-solve resets (see CostArgs)
+        if (A.err && threadIdx.x == 0) *A.err = 0;
+        if (A.sched)
+            for (int k = threadIdx.x; k < A.sched_words; k += blockDim.x) A.sched[k] = A.sched_init[k];
+    }
     cost_chunk(A, blockIdx.x, sm);
 }
 

@@ -170,6 +170,12 @@ struct CostArgs {            // the cost-table computation (kernel parameter)
     double r;
     double* L;
     double* W;
+    // stand-alone kernel only (nullptr otherwise): CTA 0 also zeroes *err and copies the
+    // scheduler's initial state sched_init -> sched (sched_words int32) for the DP that follows
+    int32_t* err;
+    int32_t* sched;
+    const int32_t* sched_init;
+    int32_t sched_words;
 };
 
 struct CostSmem {            // its shared memory ([axis][config]: conflict-free over configs)
