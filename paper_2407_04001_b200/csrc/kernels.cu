@@ -1079,7 +1079,9 @@ backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt
         for (int k = threadIdx.x; k <= nlev; k += blockDim.x) sh_off[k] = bt_off_g[k];
         __syncthreads();
     }
-    for (int lev = 0; lev < nlev; ++lev) {
+    // a DP that reported an error (scheduler time-out) left tables unfinished: no lookups
+    const int failed = *err;
+    for (int lev = 0; lev < (failed ? 0 : nlev); ++lev) {
         for (int k = bt_off[lev] + threadIdx.x; k < bt_off[lev + 1]; k += blockDim.x) {
             const BtDesc& d = bt[k];
             int64_t idx = 0, stride = 1;
@@ -1095,7 +1097,7 @@ backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt
     // layout straight into the caller's pinned host block (mapped: no copy-engine round trip)
     int32_t* hc = host_out ? reinterpret_cast<int32_t*>(host_out + 16) : nullptr;
     for (int v = threadIdx.x; v < n; v += blockDim.x) {
-        const int32_t c = ch[v];
+        const int32_t c = failed ? 0 : ch[v];
         if (SMEM) choice[v] = c;
         if (hc) hc[v] = c;
     }
