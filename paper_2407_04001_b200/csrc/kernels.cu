@@ -858,8 +858,8 @@ void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vert
 //   list-scheduling the task DAG on the CTAs of the grid with critical-path priority (a
 //   topological order, so every task a CTA waits on is held by a running CTA: deadlock-free).
 //   A claimed task waits until pending[vertex] -- the unfinished tasks of the vertex's
-//   children -- reaches zero (relaxed polling, then one ld.acquire); its descriptors are
-//   fetched meanwhile.  A finished task decrements its parent's counter with an acq_rel RMW
+//   children -- reaches zero (relaxed spin, then fence.acq_rel: the PTX acquire pattern;
+//   multi-GPU: ld.acquire.sys); its descriptors are fetched meanwhile.  A finished task decrements its parent's counter with an acq_rel RMW
 //   after a CTA barrier, so a consumer that acquires the counter observes all child-table
 //   writes (release sequence through pending[]).
 __device__ __forceinline__ uint64_t globaltimer() {
