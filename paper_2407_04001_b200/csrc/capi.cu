@@ -583,8 +583,15 @@ pase_status prepare(pase_ctx* ctx, bool device) {
         }
     }
     widen_critical(ctx);
-    for (VertexDesc& d : ctx->vd)                         // partitioned item order (split_item)
+    for (VertexDesc& d : ctx->vd) {                       // partitioned item order (split_item)
         d.psub = (d.part && d.shape >= 0) ? (int32_t)(d.ncombo / d.radix[d.m - 1]) : 1;
+        // magic numbers of the work-item decode (division by invariant integers)
+        for (int q = 0; q < pase::kMaxDep; ++q) pase::fastdiv_magic((uint32_t)std::max(1, d.radix[q]), d.rmul[q], d.rsh[q]);
+        pase::fastdiv_magic((uint32_t)std::max<int64_t>(1, std::min<int64_t>(d.ncombo, INT32_MAX)), d.mul_combo, d.sh_combo);
+        pase::fastdiv_magic((uint32_t)std::max(1, d.ntile), d.mul_tile, d.sh_tile);
+        pase::fastdiv_magic((uint32_t)std::max(1, d.ntile2), d.mul_tile2, d.sh_tile2);
+        pase::fastdiv_magic((uint32_t)std::max(1, d.psub), d.mul_psub, d.sh_psub);
+    }
     // tasks, broadcast flags, pending counters, claim order (schedule.cpp)
     std::vector<int32_t> consumer(chunks.size());
     for (size_t k = 0; k < chunks.size(); ++k) consumer[k] = chunks[k].consumer;

@@ -210,14 +210,21 @@ __device__ __forceinline__ void combine(double& b, int& c, double ob, int oc) {
 // fastest (the warps of a CTA share a tile: L1 reuse).  Multi-GPU partitioned vertex (vd.part):
 // [combinations below the partition coordinate] fastest, then the tile, then the partition
 // coordinate -- so each rank's share of the vertex is ONE contiguous item range.
+// x / d for x < 2^31 with the host's magic numbers (VertexDesc, fastdiv_magic)
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, uint32_t mul, int sh) {
+    return (uint32_t)(((uint64_t)x * mul) >> sh);
+}
+
 __device__ __forceinline__ void split_item(const VertexDesc& vd, uint32_t it, uint32_t& combo, uint32_t& tile) {
     if (vd.part) {
-        const uint32_t S = (uint32_t)vd.psub, low = it % S, t2 = it / S;
-        tile = t2 % (uint32_t)vd.ntile;
-        combo = low + S * (t2 / (uint32_t)vd.ntile);
+        const uint32_t S = (uint32_t)vd.psub;
+        const uint32_t t2 = fdiv(it, vd.mul_psub, vd.sh_psub), low = it - t2 * S;
+        const uint32_t t3 = fdiv(t2, vd.mul_tile, vd.sh_tile);
+        tile = t2 - t3 * (uint32_t)vd.ntile;
+        combo = low + S * t3;
     } else {
-        combo = it % (uint32_t)vd.ncombo;
-        tile = it / (uint32_t)vd.ncombo;
+        tile = fdiv(it, vd.mul_combo, vd.sh_combo);
+        combo = it - tile * (uint32_t)vd.ncombo;
     }
 }
 
@@ -304,8 +311,9 @@ __device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td
         for (int c = 0; c < vd.m; ++c) {                    // mixed-radix decode (lowest fastest)
             const uint32_t r = (uint32_t)vd.radix[c];
             if (c != q) {
-                const uint32_t v = rem % r;
-                rem /= r;
+                const uint32_t qv = fdiv(rem, vd.rmul[c], vd.rsh[c]);
+                const uint32_t v = rem - qv * r;
+                rem = qv;
                 obase += (int64_t)v * ost;
 #pragma unroll
                 for (int t = 0; t < NP; ++t) pp[t] += (int64_t)v * td[t].stride[c];
@@ -429,8 +437,9 @@ __device__ __noinline__ void tile2_items(const VertexDesc& vd, const TermDesc* t
         uint32_t rem, tidx;
         split_item(vd, it, rem, tidx);
         (void)nc;
-        const int x2 = (int)(tidx % (uint32_t)vd.ntile2) * V2;
-        const int x1 = (int)(tidx / (uint32_t)vd.ntile2) * V1;
+        const uint32_t t1 = fdiv(tidx, vd.mul_tile2, vd.sh_tile2);
+        const int x2 = (int)(tidx - t1 * (uint32_t)vd.ntile2) * V2;
+        const int x1 = (int)t1 * V1;
         const int nb1 = valid ? min(V1, vd.rq - x1) : 0;
         const int nb2 = valid ? min(V2, vd.rq2 - x2) : 0;
         const double* pp[kMaxP0];
@@ -446,8 +455,9 @@ __device__ __noinline__ void tile2_items(const VertexDesc& vd, const TermDesc* t
         for (int c = 0; c < vd.m; ++c) {                    // mixed-radix decode (lowest fastest)
             const uint32_t r = (uint32_t)vd.radix[c];
             if (c != q1 && c != q2) {
-                const uint32_t v = rem % r;
-                rem /= r;
+                const uint32_t qv = fdiv(rem, vd.rmul[c], vd.rsh[c]);
+                const uint32_t v = rem - qv * r;
+                rem = qv;
                 obase += (int64_t)v * ost;
 #pragma unroll
                 for (int t = 0; t < kMaxP0; ++t) if (t < nP0) pp[t] += (int64_t)v * td[t].stride[c];
@@ -593,8 +603,9 @@ __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* 
         uint32_t rem, tidx;
         split_item(vd, it, rem, tidx);
         (void)nc;
-        const int x2 = (int)(tidx % (uint32_t)vd.ntile2) * V2;
-        const int x1 = (int)(tidx / (uint32_t)vd.ntile2) * V1;
+        const uint32_t t1 = fdiv(tidx, vd.mul_tile2, vd.sh_tile2);
+        const int x2 = (int)(tidx - t1 * (uint32_t)vd.ntile2) * V2;
+        const int x1 = (int)t1 * V1;
         const int nb1 = valid ? min(V1, vd.rq - x1) : 0;
         const int nb2 = valid ? min(V2, vd.rq2 - x2) : 0;
         // row pointers of every term at this item's combination (tiled coordinates at 0)
@@ -612,8 +623,9 @@ __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* 
         for (int c = 0; c < vd.m; ++c) {                    // mixed-radix decode (lowest fastest)
             const uint32_t r = (uint32_t)vd.radix[c];
             if (c != q1 && c != q2) {
-                const uint32_t v = rem % r;
-                rem /= r;
+                const uint32_t qv = fdiv(rem, vd.rmul[c], vd.rsh[c]);
+                const uint32_t v = rem - qv * r;
+                rem = qv;
                 obase += (int64_t)v * ost;
 #pragma unroll
                 for (int t = 0; t < NP0; ++t) pa[t] += (int64_t)v * td[t].stride[c];

@@ -47,6 +47,16 @@ struct Plan {
     uint64_t candidates = 0, entries = 0;
 };
 
+// x / d for 0 <= x < 2^31 as (x * mul) >> sh, 1 <= d < 2^31 (round-up method: with
+// 2^(s-1) < d <= 2^s, mul = ceil(2^(31+s) / d) < 2^32 and the error term stays below 2^(31+s))
+inline void fastdiv_magic(uint32_t d, uint32_t& mul, int32_t& sh) {
+    int s = 0;
+    while ((1ull << s) < d) ++s;
+    const unsigned __int128 num = (unsigned __int128)1 << (31 + s);
+    mul = (uint32_t)((num + d - 1) / d);
+    sh = 31 + s;
+}
+
 // Builds a Plan.  Returns PASE_OK or an error with a message.
 pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* m, Plan& plan,
                        std::string& err);
@@ -109,6 +119,13 @@ struct VertexDesc {          // one DP vertex (rank i)
     int32_t ntasks;          // persistent schedule: this rank's tasks of the vertex ...
     int32_t task0;           // ... with local ids [task0, task0 + ntasks)
     int32_t parent;          // rank of the elimination-tree parent (-1: root)
+    // division by invariant integers (decode of work items): x / d == (x * mul) >> sh for
+    // x < 2^31 (magic numbers from fastdiv_magic on the host), per coordinate radix and for
+    // ncombo, ntile, ntile2, psub
+    uint32_t rmul[kMaxDep];
+    int32_t rsh[kMaxDep];
+    uint32_t mul_combo, mul_tile, mul_tile2, mul_psub;
+    int32_t sh_combo, sh_tile, sh_tile2, sh_psub;
     int32_t part;            // multi-GPU: table partitioned by its top coordinate
     int32_t psub;            // partitioned: combinations below the top coordinate (ncombo / K_top)
     int32_t bcast;           // bit 0: write T to every rank, bit 1: write A to every rank
