@@ -949,12 +949,13 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
     fill_stats(ctx);
     using ms = std::chrono::duration<double, std::milli>;
     ctx->stats.ms_create = ms(t_graph - t0).count();
-    if (const char* tv = std::getenv("PASE_TIMING"); tv && tv[0] == '1')
+    if (const char* tv = std::getenv("PASE_TIMING"); tv && tv[0] == '1') {
         std::fprintf(stderr, "[pase] pools %p (%zu B) %p (%zu B), T at %p\n", ctx->pool, ctx->pool_bytes, ctx->pool2,
                      ctx->pool2_bytes, (void*)ctx->d_T);
         std::fprintf(stderr, "[pase] create: plan+setup %.3f ms, alloc %.3f ms, upload %.3f ms, graph %.3f ms\n",
                      ms(t_plan - t0).count(), ms(t_alloc - t_plan).count(), ms(t_upload - t_alloc).count(),
                      ms(t_graph - t_upload).count());
+    }
     *out = ctx;
     return PASE_OK;
 }
