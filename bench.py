@@ -348,7 +348,7 @@ def main():
                       "solve_total": statistics.mean(step_ms)},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
-                     "kernel": "dp_fill (all launches of the DP phase, CUDA events in the solve graph)",
+                     "kernel": "dp_persistent (the whole DP phase is one persistent launch; timed by CUDA event nodes in the solve graph)",
                      "peak_source": f"derived: {SM_COUNT} SM x {FP64_LANES_PER_SM} fp64 lanes x {sm_mhz:.0f} MHz (DESIGN §5)",
                      "hbm_view": {"achieved_gbs": hbm_achieved, "peak_gbs": hbm_peak,
                                   "frac": hbm_achieved / hbm_peak, "alg_bytes": int(st["alg_bytes_dp"])}},
