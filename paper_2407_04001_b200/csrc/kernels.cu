@@ -1,6 +1,8 @@
 // kernels.cu -- sm_100a kernels of the PaSE hot path.
 //   K1 cost_tables   (row a5): L_v[C] = t_l(v, C, r), W_e = r * t_x (Eq. 1)
-//   K2 dp_fill       (row a6): Eq. 4 / Fig. 5 lines 8-20
+//   K2 dp_persistent (row a6): Eq. 4 / Fig. 5 lines 8-20 over the whole
+//                    elimination tree in one launch (tile families: DESIGN §5.2; schedule: §5.3);
+//                    dp_fill_vertex runs one vertex per launch (PASE_SCHEDULE=launches)
 //   K3 backtrack     (row a7): back-substitution from sigma_|V|.cfg
 // Bit-exactness rules: every fp64 op is an explicit IEEE RN intrinsic
 // (__dadd_rn / __dmul_rn / __ddiv_rn / __ull2double_rn), never contracted to FMA; the sum
@@ -189,7 +191,7 @@ void launch_cost_tables(const CostArgs& A, int nchunks, void* stream) {
 }
 
 // =====================================================================================
-// K2: DP fill, tiled (DESIGN §4.2).
+// K2: DP fill, tiled (DESIGN §5.2).
 //   Work item = one combination of the D(i) coordinates other than qstar, times a tile of
 //   up to kTile consecutive values of qstar.  A lane group of G lanes splits the reduction
 //   over C (lane l takes C = l, l+G, ...; loads of every table row are coalesced over C).
