@@ -5,12 +5,17 @@
  * Build: gcc -O2 -std=c99 -ffp-contract=off -fopenmp -shared -fPIC oracle.c -o liboracle.so
  * (-ffp-contract=off: every fp64 operation below is one IEEE round-to-nearest op.)
  *
- * Pins (tests/test_oracle_*.py): brute force (Theorem 1), definitional
+ * Pins (tests/test_oracle*.py): brute force (Theorem 1), definitional
  * dependent sets (Theorem 2), the Fig. 3 worked example,
- * hand-computed GEMM/data-parallel closed forms, path-graph Viterbi, tree message
- * passing, r=0 separability, the Appendix-A telescoping identity.
- * Parity UNPINNED: the absolute t_l / t_x formulas, which the
- * paper does not publish; they are pinned only by closed forms.
+ * hand-computed closed forms (tests/golden/closed_forms.json: GEMM data-parallel and
+ * column-split t_l / t_x, the conv halo term over the input-tensor axes, t_x with an
+ * axis the consumer does not split, the MLP / AlexNet candidate counts), path-graph
+ * Viterbi, tree message passing, r=0 separability, the Appendix-A telescoping identity
+ * (P:1206-1214).  Every branch of t_l (compute, reduction AR, gradient AR, halo) and of
+ * t_x (mapped, unmapped axis) has a hand-derived value.  What stays a READING, not a
+ * paper number: the paper does not publish its t_l / t_x formulas
+ * (P:268-270), so these closed forms pin the oracle to our reading of Eq. 1, not to the
+ * paper's unpublished code.
  */
 #include "oracle.h"
 
@@ -39,6 +44,8 @@ static int nd_nhalo(const int64_t* r) { return (int)r[30]; }
 static int nd_halo_h(const int64_t* r, int q) { return (int)r[31 + q]; }
 static int nd_halo_r(const int64_t* r, int q) { return (int)r[35 + q]; }
 static int64_t nd_elem(const int64_t* r) { return r[39]; }
+static int nd_nin(const int64_t* r) { return (int)r[40]; }
+static int nd_in(const int64_t* r, int a) { return (int)r[41 + a]; }
 
 /* ---------------------------------------------------------------- validation */
 int or_validate(int n, const int64_t* nodes, int m, const int64_t* edges)
@@ -59,10 +66,19 @@ int or_validate(int n, const int64_t* nodes, int m, const int64_t* edges)
             if (nd_w(r, a) < 0 || nd_w(r, a) >= d) return 1;
             for (int b = 0; b < a; ++b) if (nd_w(r, a) == nd_w(r, b)) return 1;
         }
+        if (nd_nin(r) < 0 || nd_nin(r) > d) return 1;
+        for (int a = 0; a < nd_nin(r); ++a) {
+            if (nd_in(r, a) < 0 || nd_in(r, a) >= d) return 1;
+            for (int b = 0; b < a; ++b) if (nd_in(r, a) == nd_in(r, b)) return 1;
+        }
         if (nd_nhalo(r) < 0 || nd_nhalo(r) > 4) return 1;
         for (int q = 0; q < nd_nhalo(r); ++q) {
             if (nd_halo_h(r, q) < 0 || nd_halo_h(r, q) >= d) return 1;
             if (nd_halo_r(r, q) < 0 || nd_halo_r(r, q) >= d) return 1;
+            /* the halo runs along an axis of the input tensor (reading L) */
+            int found = 0;
+            for (int a = 0; a < nd_nin(r); ++a) if (nd_in(r, a) == nd_halo_h(r, q)) found = 1;
+            if (!found) return 1;
         }
         if (nd_elem(r) < 1 || nd_fpp(r) < 0) return 1;
     }
@@ -188,13 +204,16 @@ static double layer_cost(const int64_t* r, const int32_t* c, double ratio)
     int64_t out_bytes = nd_elem(r) * out_elems;
     int64_t w_bytes = (nd_nw(r) > 0) ? nd_elem(r) * w_elems : 0;
     if (nd_nw(r) == 0) g_grad = 1;
+    /* conv halo (reading L): a split spatial dim h paired with filter dim f exchanges
+     * (size_f - 1) input rows per shard; a row is the face of the INPUT-tensor shard across h,
+     * i.e. the product of the input-tensor axes other than h; x2 for fwd + bwd */
     int64_t halo = 0;
     for (int q = 0; q < nd_nhalo(r); ++q) {
         int h = nd_halo_h(r, q), f = nd_halo_r(r, q);
         if (c[h] > 1 && nd_size(r, f) > 1) {
             int64_t face = 1;
-            for (int a = 0; a < nd_nout(r); ++a)
-                if (nd_out(r, a) != h) face *= s[nd_out(r, a)];
+            for (int a = 0; a < nd_nin(r); ++a)
+                if (nd_in(r, a) != h) face *= s[nd_in(r, a)];
             halo += 2 * nd_elem(r) * (nd_size(r, f) - 1) * face;
         }
     }

@@ -15,7 +15,8 @@
  *     [10] n_out  [11..18] out_axes  [19] n_w  [20..27] w_axes
  *     [28] flop_dims bitmask (0 = all dims)  [29] flops_per_point
  *     [30] n_halo [31..34] halo spatial dims [35..38] halo filter dims
- *     [39] elem_bytes
+ *     [39] elem_bytes  [40] n_in  [41..48] in_axes (iteration dims of the input-tensor axes;
+ *     the conv halo face runs over them, DESIGN reading L)
  *   edge record, OR_EDGE_REC int64 fields: [0] src [1] dst [2..9] axis_map (-1 = none)
  *
  * Cost tables (memoised t_l / t_x, SURVEY §8.c.1 "Implementation notes"):
@@ -27,7 +28,7 @@
 #include <stdint.h>
 
 #define OR_MAXD 8
-#define OR_NODE_REC 40
+#define OR_NODE_REC 49
 #define OR_EDGE_REC 10
 
 #ifdef __cplusplus

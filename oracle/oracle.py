@@ -17,7 +17,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "liboracle.so")
-MAXD, NODE_REC, EDGE_REC = 8, 40, 10
+MAXD, NODE_REC, EDGE_REC = 8, 49, 10
 EXACT_P, LE_P = 0, 1
 
 
@@ -69,7 +69,7 @@ def _p(a: np.ndarray, ct):
 
 
 def encode(graph: dict) -> Tuple[np.ndarray, np.ndarray]:
-    """Graph dict -> (node records int64[n, 40], edge records int64[m, 10])."""
+    """Graph dict -> (node records int64[n, 49], edge records int64[m, 10])."""
     nodes = graph["nodes"]
     N = np.zeros((len(nodes), NODE_REC), dtype=np.int64)
     for v, nd in enumerate(nodes):
@@ -94,6 +94,9 @@ def encode(graph: dict) -> Tuple[np.ndarray, np.ndarray]:
         for q, (h, f) in enumerate(halo):
             r[31 + q], r[35 + q] = h, f
         r[39] = nd.get("elem_bytes", 4)
+        ins = nd.get("in_axes") or []
+        r[40] = len(ins)
+        r[41:41 + len(ins)] = ins
     edges = graph["edges"]
     E = np.full((max(len(edges), 1), EDGE_REC), -1, dtype=np.int64)
     for e, ed in enumerate(edges):

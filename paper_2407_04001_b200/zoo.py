@@ -12,6 +12,8 @@ DESIGN.md §3 (an extension of SPEC.md:97 "JSON graph schema"):
             "flop_dims": null | [iter-dim indices]          (null = all dims),
             "flops_per_point": int,                         (fwd+bwd FLOPs per iteration point)
             "halo": [[spatial_dim, filter_dim], ...],       (conv halo pairs)
+            "in_axes":  [iter-dim index per input-tensor axis] ([] = not given; required with a
+                                                             halo: the halo face, DESIGN reading L)
             "elem_bytes": int}
     edge = {"src", "dst", "axis_map": [dst iter-dim per src output axis, -1 = none]}
     graph = {"nodes": [...], "edges": [...], "machine": {"flops": F, "bandwidth": B}}
@@ -38,7 +40,7 @@ class GraphBuilder:
     def node(self, name: str, kind: str, dims: Sequence[Tuple], out: Sequence[str],
              w: Sequence[str] = (), fpp: int = 2, flop_dims: Optional[Sequence[str]] = None,
              halo: Sequence[Tuple[str, str]] = (), elem_bytes: int = 4,
-             unsplittable: Iterable[str] = ()) -> int:
+             unsplittable: Iterable[str] = (), inp: Sequence[str] = ()) -> int:
         names = [d[0] for d in dims]
         assert len(set(names)) == len(names), f"duplicate dim names in {name}"
         nosplit = set(unsplittable)
@@ -56,6 +58,7 @@ class GraphBuilder:
             "flops_per_point": int(fpp),
             "halo": [[idx[h], idx[r]] for h, r in halo],
             "elem_bytes": int(elem_bytes),
+            "in_axes": [idx[a] for a in inp],
         })
         return nid
 
@@ -107,7 +110,7 @@ def _conv(g: GraphBuilder, name: str, b: int, cin: int, h: int, w: int, cout: in
     return g.node(name, "conv2d",
                   [("b", b), ("c", cin), ("h", h), ("w", w), ("n", cout), ("r", r), ("s", s)],
                   out=["b", "n", "h", "w"], w=["c", "n", "r", "s"], fpp=6,
-                  halo=[("h", "r"), ("w", "s")], unsplittable=("r", "s"))
+                  halo=[("h", "r"), ("w", "s")], unsplittable=("r", "s"), inp=["b", "c", "h", "w"])
 
 
 def _pool(g: GraphBuilder, name: str, b: int, c: int, h: int, w: int, r: int, s: int) -> int:
@@ -508,6 +511,7 @@ def random_model_graph(n: int, seed: int, extra_p: float = 0.3, max_log: int = 4
     unsplittable), random output / weight axes, random axis maps and halos: exercises
     the cost model (t_l, t_x) on structures the zoo does not produce."""
     rng = random.Random(seed * 104729 + 3)
+    rng_in = random.Random(seed * 7 + 11)          # input-tensor axes (own stream: same graphs)
     g = GraphBuilder()
     names = "abcdefgh"
     for i in range(n):
@@ -526,8 +530,11 @@ def random_model_graph(n: int, seed: int, extra_p: float = 0.3, max_log: int = 4
         halo = []
         if d >= 2 and rng.random() < 0.2:
             halo = [(dn[0], dn[1])]
+        inp = rng_in.sample(dn, rng_in.randint(1, d))
+        if halo and dn[0] not in inp:
+            inp = [dn[0]] + inp[:d - 1]
         g.node(f"m{i}", "synthetic", dims, out=out, w=w, fpp=rng.choice([1, 2, 6, 10]),
-               flop_dims=fd, halo=halo, elem_bytes=rng.choice([2, 4]))
+               flop_dims=fd, halo=halo, elem_bytes=rng.choice([2, 4]), inp=inp)
     for a, c in random_topology(n, seed, extra_p, multi_p):
         src, dst = g.nodes[a], g.nodes[c]
         dnames = [x["name"] for x in dst["dims"]]

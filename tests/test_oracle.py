@@ -363,3 +363,63 @@ def test_bfs_guard_trips_on_inception():
     assert ei.value.code == 2
     off, _ = P.table_sizes(order=0)
     assert off[-1] < 10 ** 8
+
+
+# --------------------------------------------------------------------------- reading L / K / counts
+def _node(g, name):
+    return [n["name"] for n in g["nodes"]].index(name)
+
+
+def test_conv_halo_closed_form():
+    """P:228 'halo communication for convolutions', reading L: the face of a split spatial dim
+    runs over the INPUT-tensor axes (b, c, w for h).  Hand-derived values (golden); the second
+    config splits c and n, so a face over the output axes (s_n instead of s_c) fails it."""
+    gold = json.load(open(os.path.join(GOLD, "closed_forms.json")))["conv_halo_inception_mixed_7b_b2_3x3"]
+    g = zoo.inception_v3()
+    v = _node(g, gold["node"])
+    cf = [tuple(c) for c in O.configs(g, gold["p"])[v]]
+    K, Ls, _ = O.cost_tables(g, gold["p"])
+    for key, tup in (("config_16_1_2_1_1_1_1", (16, 1, 2, 1, 1, 1, 1)), ("config_4_2_2_1_2_1_1", (4, 2, 2, 1, 2, 1, 1))):
+        assert Ls[v][cf.index(tup)] == gold[key]["t_l"], key
+    # no halo when the spatial dims are unsplit, whatever else is split
+    c0 = cf.index((32, 1, 1, 1, 1, 1, 1))
+    w_bytes = 4 * 448 * 384 * 9
+    assert Ls[v][c0] == 2378170368 + 1000.0 * (2 * 31 * w_bytes // 32)
+
+
+def test_tx_unmapped_axis_closed_form():
+    """P:271-276, reading K: an axis the consumer does not split (axis_map -1) is needed whole."""
+    gold = json.load(open(os.path.join(GOLD, "closed_forms.json")))["tx_unmapped_axis_alexnet_pool3_fc1"]
+    g = zoo.alexnet()
+    a, b = _node(g, "pool3"), _node(g, "fc1")
+    e = [i for i, ed in enumerate(g["edges"]) if ed["src"] == a and ed["dst"] == b][0]
+    assert g["edges"][e]["axis_map"][2:] == [-1, -1]
+    cf = O.configs(g, gold["p"])
+    K, Ls, Ws = O.cost_tables(g, gold["p"])
+    ia = [tuple(c) for c in cf[a]].index((1, 4, 2, 1, 1, 1))
+    ib = [tuple(c) for c in cf[b]].index((1, 1, 8))
+    assert Ws[e][ia, ib] == gold["W"]
+    # producer with unsplit h, w holds everything the flatten needs along them: only c matters
+    ia2 = [tuple(c) for c in cf[a]].index((1, 8, 1, 1, 1, 1))
+    assert Ws[e][ia2, ib] == 0.0
+
+
+def test_candidate_counts_closed_form():
+    """Sum_i K(sigma_i)|T(i)| of the two brute-force-sized BASELINE configs (hand-derived)."""
+    gold = json.load(open(os.path.join(GOLD, "closed_forms.json")))["candidate_counts"]
+    for name, key in (("mlp", "mlp_p4"), ("alexnet", "alexnet_p8")):
+        g, p = zoo.bench_graph(name)
+        K = np.array([len(c) for c in O.configs(g, p)], np.int32)
+        assert list(K) == gold[key]["K"], name
+        P = O.Problem(g, K, [np.zeros(k) for k in K], [np.zeros((K[e["src"]], K[e["dst"]])) for e in g["edges"]])
+        assert P.table_sizes()[1] == gold[key]["candidates"], name
+
+
+def test_halo_requires_input_axes():
+    """Reading L: a halo pair must name a spatial dim of the input tensor."""
+    g = zoo.GraphBuilder()
+    g.node("c", "conv2d", [("b", 8), ("h", 8), ("r", 3)], out=["b", "h"], halo=[("h", "r")], inp=["b"])
+    assert O.validate(g.graph()) == 1
+    g = zoo.GraphBuilder()
+    g.node("c", "conv2d", [("b", 8), ("h", 8), ("r", 3)], out=["b", "h"], halo=[("h", "r")], inp=["b", "h"])
+    assert O.validate(g.graph()) == 0
