@@ -79,6 +79,13 @@ typedef struct {
     int32_t halo_spatial[PASE_MAX_HALO];   /* spatial iteration dim h ... */
     int32_t halo_filter[PASE_MAX_HALO];    /* ... paired with filter dim r */
     int32_t elem_bytes;                    /* bytes per tensor element, >= 1 */
+    int32_t n_in_axes;                     /* input tensor rank, 0..n_dims (0 = not given) */
+    int32_t in_axes[PASE_MAX_DIMS];        /* iteration dim of each input-tensor axis (distinct; conv:
+                                              b, c, h, w).  The halo of pair q exchanges
+                                              (size[r] - 1) input rows whose face is the product of the
+                                              shard extents of the input axes other than h (DESIGN
+                                              reading L); every halo_spatial[q] must be one of
+                                              them, else PASE_ERR_INVALID */
 } pase_node;
 
 /* Tensor flowing src -> dst.  axis_map[a] = dst iteration dim aligned with
@@ -144,7 +151,10 @@ typedef struct pase_ctx pase_ctx;
 pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, pase_ctx** out);
 
 /* a5-a8: runs the whole search on the GPU (cost tables, DP fill over the elimination tree,
- * back-substitution).  configs_out: caller-allocated int32[n_nodes * PASE_MAX_DIMS], row v =
+ * back-substitution).  Scheduler and group-barrier waits are bounded by PASE_SPIN_TIMEOUT_MS
+ * (environment at pase_create, default 4000, 0 = unbounded): a wait past it fails the solve
+ * with PASE_ERR_STATE instead of hanging; a DP entry with no finite candidate (fp64 overflow
+ * of a sum) fails it with PASE_ERR_RESOURCE.  configs_out: caller-allocated int32[n_nodes * PASE_MAX_DIMS], row v =
  * the split tuple of node v (unused dims = 1); may be NULL.  config_index_out: int32[n_nodes]
  * index of phi*(v) in C(v) (lexicographic order); may be NULL.  total_cost_out: f(|V|, ∅).
  * May be called repeatedly; every call recomputes everything. */
@@ -171,13 +181,18 @@ pase_status pase_get_order(const pase_ctx* ctx, int32_t* sigma, int32_t* dep_off
 pase_status pase_get_cost_tables(const pase_ctx* ctx, int32_t index, int32_t is_edge, double* out);
 
 /* T(i) and A(i) of rank i after pase_solve (|T(i)| entries; coordinates D(i) ascending rank,
- * lowest rank fastest).  On multi-GPU contexts the partitions are gathered. */
+ * lowest rank fastest).  On a connected multi-GPU context the other ranks' slices of a
+ * partitioned T(i) are gathered from their pools through the peer mappings (A(i) is complete
+ * on every rank).  PASE_ERR_STATE between pase_launch and pase_finish. */
 pase_status pase_get_dp_table(const pase_ctx* ctx, int32_t rank, double* T_out, uint16_t* A_out);
 int64_t pase_table_entries(const pase_ctx* ctx, int32_t rank);
 
 /* Replace the cost model by explicit tables (synthetic-cost tests): L concatenated
  * over nodes in id order (K_v each), W over edges in id order (K_src*K_dst each, src-major).
- * Subsequent pase_solve calls use these tables instead of running the cost-table kernel. */
+ * Subsequent pase_solve calls use these tables instead of running the cost-table kernel.
+ * Every value must be finite (PASE_ERR_INVALID names the first that is not); PASE_ERR_STATE
+ * between pase_launch and pase_finish.  The copy is ordered on the context's stream and
+ * complete when the call returns. */
 pase_status pase_set_cost_tables(pase_ctx* ctx, const double* L, const double* W);
 
 /* Persistent-schedule timeline (tracing; enabled by env PASE_TRACE=1 at pase_create): per DP

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -71,11 +72,13 @@ struct pase_ctx {
     int64_t* d_trace = nullptr;             // PASE_TRACE=1: kTraceWords int64 per persistent task
     int ntasks = 0, nblocks = 0;
     int64_t total_tasks = 0;
+    uint64_t timeout_ns = 4000000000ull;    // scheduler / barrier wait limit (PASE_SPIN_TIMEOUT_MS)
     bool persistent = true;
     bool cost_tasks = false;                // persistent: cost tables as tasks of the DP kernel
     // multi-GPU
     pase::Peers peers{};
     bool connected = false;
+    std::vector<double*> peer_T;            // every rank's T pool (index = rank), after connect
     std::vector<void*> ipc_opened;
     // host mirrors
     std::vector<VertexDesc> vd;
@@ -642,6 +645,7 @@ pase_status prepare(pase_ctx* ctx, bool device) {
             b.A = ctx->vd[i].A;
             b.node = P.sigma[i];
             b.m = (int32_t)P.dep[i].size();
+            b.K = P.K[P.sigma[i]];
             for (int a = 0; a < b.m; ++a) { b.dep[a] = P.dep[i][a]; b.radix[a] = P.K[P.dep[i][a]]; }
         }
     }
@@ -726,11 +730,11 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
     if (ctx->persistent) {
         if (!fold)
             CUDA_TRY(cudaMemcpyAsync(ctx->d_sched, ctx->d_sched_init, ctx->sched_bytes, cudaMemcpyDeviceToDevice, s));
-        if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, s);
+        if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, ctx->timeout_ns, s);
         pase::launch_dp_persistent(ctx->d_vd, ctx->d_td, ctx->d_tasks, ctx->d_order, ctx->ntasks, ctx->d_sched,
                                    d_err, ctx->peers, cost_args(ctx), ctx->nblocks,
-                                   trace_on() ? ctx->d_trace : nullptr, s);
-        if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, s);
+                                   trace_on() ? ctx->d_trace : nullptr, ctx->timeout_ns, s);
+        if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, ctx->timeout_ns, s);
     } else {
         CUDA_TRY(cudaEventRecord(start, s));
         std::vector<int> sid(n, -1);                      // a chain stays on one stream
@@ -825,7 +829,7 @@ void fill_stats(pase_ctx* ctx) {
 struct HandleBlob {
     uint32_t magic;
     int32_t version;
-    int64_t pid;
+    uint64_t nonce;                     // random per process: same-process peers (virtual ranks)
     int32_t device, world, rank, n;
     int64_t total_tasks;
     cudaIpcMemHandle_t h1, h2;
@@ -834,6 +838,22 @@ struct HandleBlob {
 };
 static_assert(sizeof(HandleBlob) <= PASE_HANDLE_BYTES, "handle blob too large");
 constexpr uint32_t kMagic = 0x50415345;   // "PASE"
+
+// Identifies this process among the group's (a bare pid can repeat across PID namespaces on one
+// node): drawn once from the OS entropy source, mixed with the pid and the clock.
+uint64_t process_nonce() {
+    static const uint64_t nonce = [] {
+        uint64_t x = 0;
+        if (FILE* f = std::fopen("/dev/urandom", "rb")) {
+            if (std::fread(&x, sizeof x, 1, f) != 1) x = 0;
+            std::fclose(f);
+        }
+        x ^= (uint64_t)getpid() * 0x9e3779b97f4a7c15ull;
+        x ^= (uint64_t)std::chrono::steady_clock::now().time_since_epoch().count();
+        return x | 1ull;
+    }();
+    return nonce;
+}
 
 }  // namespace
 
@@ -856,6 +876,8 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
         return PASE_ERR_INVALID;
     }
     ctx->dev = m->cuda_device;
+    if (const char* to = std::getenv("PASE_SPIN_TIMEOUT_MS"))      // 0 = wait without limit
+        ctx->timeout_ns = (uint64_t)std::max(0ll, std::atoll(to)) * 1000000ull;
     auto fail = [&](pase_status code) {
         g_create_err = ctx->err;
         pase_destroy(ctx);
@@ -991,9 +1013,11 @@ pase_status pase_finish(pase_ctx* ctx, int32_t* configs_out, int32_t* config_ind
     CUDA_TRY(cudaSetDevice(ctx->dev));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     if (*ctx->h_err) {
-        ctx->err = std::string("scheduler wait timed out (code ") + std::to_string(*ctx->h_err) +
-                   "): ranks of the group not running concurrently?";
-        return PASE_ERR_STATE;
+        const int code = *ctx->h_err;
+        ctx->err = code == 3 ? std::string("DP entry without a finite candidate (cost overflow): no strategy")
+                             : std::string("scheduler wait timed out after PASE_SPIN_TIMEOUT_MS (code ") +
+                                   std::to_string(code) + "): ranks of the group not running concurrently?";
+        return code == 3 ? PASE_ERR_RESOURCE : PASE_ERR_STATE;
     }
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
@@ -1029,7 +1053,7 @@ pase_status pase_export_handle(const pase_ctx* ctx_c, void* blob) {
     HandleBlob h{};
     h.magic = kMagic;
     h.version = 1;
-    h.pid = (int64_t)getpid();
+    h.nonce = process_nonce();
     h.device = ctx->dev;
     h.world = ctx->world;
     h.rank = ctx->rank;
@@ -1070,7 +1094,7 @@ pase_status pase_connect(pase_ctx* ctx, const void* blobs) {
         if (q == ctx->rank) {
             b1 = (char*)ctx->pool;
             b2 = (char*)ctx->pool2;
-        } else if (h.pid == (int64_t)getpid()) {        // virtual ranks in one process
+        } else if (h.nonce == process_nonce()) {        // virtual ranks in one process
             b1 = (char*)(uintptr_t)h.raw1;
             b2 = (char*)(uintptr_t)h.raw2;
             if (h.device != ctx->dev) {
@@ -1105,7 +1129,12 @@ pase_status pase_connect(pase_ctx* ctx, const void* blobs) {
             ++k;
         }
     }
-    CUDA_TRY(cudaMemcpy(ctx->d_vd, ctx->vd.data(), sizeof(VertexDesc) * ctx->P.n, cudaMemcpyHostToDevice));
+    // ordered on the context's stream (the solves run there), complete before return: vd is
+    // pageable host memory
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_vd, ctx->vd.data(), sizeof(VertexDesc) * ctx->P.n, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    ctx->peer_T = Tb;
     ctx->connected = true;
     return record_graph(ctx);
 }
@@ -1202,17 +1231,22 @@ pase_status pase_get_cost_tables(const pase_ctx* ctx_c, int32_t index, int32_t i
     if (ctx->dev < 0) { ctx->err = "host-only planning context has no device tables"; return PASE_ERR_STATE; }
     const Plan& P = ctx->P;
     if (!ctx->solved && !ctx->override_tables) { ctx->err = "call pase_solve first"; return PASE_ERR_STATE; }
+    if (ctx->launched) { ctx->err = "pase_get_cost_tables during a launched solve"; return PASE_ERR_STATE; }
     CUDA_TRY(cudaSetDevice(ctx->dev));
     if (!is_edge) {
         if (index < 0 || index >= P.n) return PASE_ERR_INVALID;
-        CUDA_TRY(cudaMemcpy(out, ctx->d_L + P.loff[index], sizeof(double) * P.K[index], cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpyAsync(out, ctx->d_L + P.loff[index], sizeof(double) * P.K[index], cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         return PASE_OK;
     }
     if (index < 0 || index >= P.m) return PASE_ERR_INVALID;
     const pase_edge& e = P.edges[index];
     const int ks = P.K[e.src], kd = P.K[e.dst];
     std::vector<double> buf((size_t)ks * kd);
-    CUDA_TRY(cudaMemcpy(buf.data(), ctx->d_W + P.woff[index], sizeof(double) * buf.size(), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpyAsync(buf.data(), ctx->d_W + P.woff[index], sizeof(double) * buf.size(), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     const bool later_is_src = P.rank[e.src] > P.rank[e.dst];
     for (int cs = 0; cs < ks; ++cs)
         for (int cd = 0; cd < kd; ++cd)
@@ -1230,31 +1264,59 @@ pase_status pase_get_dp_table(const pase_ctx* ctx_c, int32_t rank, double* T_out
     if (!ctx || rank < 0 || rank >= ctx->P.n) return PASE_ERR_INVALID;
     if (ctx->dev < 0) { ctx->err = "host-only planning context has no device tables"; return PASE_ERR_STATE; }
     if (!ctx->solved) { ctx->err = "call pase_solve first"; return PASE_ERR_STATE; }
+    if (ctx->launched) { ctx->err = "pase_get_dp_table during a launched solve"; return PASE_ERR_STATE; }
     CUDA_TRY(cudaSetDevice(ctx->dev));
     const int64_t sz = ctx->P.tsize[rank], off = ctx->P.toff[rank];
-    if (T_out) CUDA_TRY(cudaMemcpy(T_out, ctx->d_T + off, sizeof(double) * sz, cudaMemcpyDeviceToHost));
-    if (A_out) CUDA_TRY(cudaMemcpy(A_out, ctx->d_A + off, sizeof(uint16_t) * sz, cudaMemcpyDeviceToHost));
+    if (T_out) CUDA_TRY(cudaMemcpyAsync(T_out, ctx->d_T + off, sizeof(double) * sz, cudaMemcpyDeviceToHost, ctx->stream));
+    if (A_out) CUDA_TRY(cudaMemcpyAsync(A_out, ctx->d_A + off, sizeof(uint16_t) * sz, cudaMemcpyDeviceToHost, ctx->stream));
+    // multi-GPU: a partitioned table whose T is not broadcast holds only this rank's slice
+    // (configs [q K/G, (q+1) K/G) of its top coordinate, the slowest): gather the others'
+    // slices from their pools through the peer mappings (argmin tables are always complete)
+    const VertexDesc& d = ctx->vd[rank];
+    if (T_out && ctx->world > 1 && d.part && !(d.bcast & 1) && ctx->connected) {
+        const int64_t Kt = d.radix[d.m - 1], S = sz / Kt;
+        for (int q = 0; q < ctx->world; ++q) {
+            if (q == ctx->rank) continue;
+            const int64_t lo = q * Kt / ctx->world * S, hi = (q + 1) * Kt / ctx->world * S;
+            if (hi > lo)
+                CUDA_TRY(cudaMemcpyAsync(T_out + lo, ctx->peer_T[q] + off + lo, sizeof(double) * (hi - lo),
+                                         cudaMemcpyDefault, ctx->stream));
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return PASE_OK;
 }
 
 pase_status pase_set_cost_tables(pase_ctx* ctx, const double* L, const double* W) {
     if (!ctx || !L || (!W && ctx->P.m > 0)) return PASE_ERR_INVALID;
     if (ctx->dev < 0) { ctx->err = "host-only planning context has no device tables"; return PASE_ERR_STATE; }
+    if (ctx->launched) { ctx->err = "pase_set_cost_tables during a launched solve"; return PASE_ERR_STATE; }
     const Plan& P = ctx->P;
+    // Eq. 1 costs are finite (a non-finite candidate would leave a DP entry without argmin)
+    for (int64_t k = 0; k < P.loff[P.n]; ++k)
+        if (!std::isfinite(L[k])) { ctx->err = "pase_set_cost_tables: L[" + std::to_string(k) + "] is not finite"; return PASE_ERR_INVALID; }
+    for (int64_t k = 0; k < P.woff[P.m]; ++k)
+        if (!std::isfinite(W[k])) { ctx->err = "pase_set_cost_tables: W[" + std::to_string(k) + "] is not finite"; return PASE_ERR_INVALID; }
     CUDA_TRY(cudaSetDevice(ctx->dev));
-    CUDA_TRY(cudaMemcpy(ctx->d_L, L, sizeof(double) * P.loff[P.n], cudaMemcpyHostToDevice));
-    std::vector<double> buf;
+    // one pageable staging buffer in the device layout, copied on the context's stream (the
+    // solves' stream) and complete before return
+    std::vector<double> buf((size_t)(P.loff[P.n] + P.woff[P.m]));
+    std::memcpy(buf.data(), L, sizeof(double) * P.loff[P.n]);
     for (int e = 0; e < P.m; ++e) {          // src-major input -> [later][earlier] device layout
         const pase_edge& x = P.edges[e];
         const int ks = P.K[x.src], kd = P.K[x.dst];
         const double* w = W + P.woff[e];
-        buf.resize((size_t)ks * kd);
+        double* o = buf.data() + P.loff[P.n] + P.woff[e];
         const bool later_is_src = P.rank[x.src] > P.rank[x.dst];
         for (int cs = 0; cs < ks; ++cs)
             for (int cd = 0; cd < kd; ++cd)
-                (later_is_src ? buf[(size_t)cs * kd + cd] : buf[(size_t)cd * ks + cs]) = w[(size_t)cs * kd + cd];
-        CUDA_TRY(cudaMemcpy(ctx->d_W + P.woff[e], buf.data(), sizeof(double) * buf.size(), cudaMemcpyHostToDevice));
+                (later_is_src ? o[(size_t)cs * kd + cd] : o[(size_t)cd * ks + cs]) = w[(size_t)cs * kd + cd];
     }
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_L, buf.data(), sizeof(double) * P.loff[P.n], cudaMemcpyHostToDevice, ctx->stream));
+    if (P.m > 0)
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_W, buf.data() + P.loff[P.n], sizeof(double) * P.woff[P.m],
+                                 cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     if (!ctx->override_tables) {
         ctx->override_tables = true;
         pase_status st = record_graph(ctx);
@@ -1267,7 +1329,9 @@ int64_t pase_get_trace(const pase_ctx* ctx_c, int64_t* out, int64_t cap) {
     pase_ctx* ctx = const_cast<pase_ctx*>(ctx_c);
     if (!ctx || ctx->dev < 0 || !ctx->d_trace || !trace_on()) return 0;
     const int64_t nt = std::min<int64_t>(ctx->ntasks, cap);
-    if (out && nt > 0 && cudaMemcpy(out, ctx->d_trace, sizeof(int64_t) * pase::kTraceWords * nt, cudaMemcpyDeviceToHost) != cudaSuccess)
+    if (out && nt > 0 && (cudaMemcpyAsync(out, ctx->d_trace, sizeof(int64_t) * pase::kTraceWords * nt,
+                                          cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+                          cudaStreamSynchronize(ctx->stream) != cudaSuccess))
         return -1;
     return ctx->ntasks;
 }

@@ -47,10 +47,22 @@ pase_status validate(const pase_graph* g, std::string& err) {
             if (d < 0 || d >= x.n_dims || (seen >> d & 1u)) { err = fmt("node %lld: bad weight axis %lld", v, a); return PASE_ERR_INVALID; }
             seen |= 1u << d;
         }
+        if (x.n_in_axes < 0 || x.n_in_axes > x.n_dims) { err = fmt("node %lld: bad n_in_axes", v); return PASE_ERR_INVALID; }
+        seen = 0;
+        for (int a = 0; a < x.n_in_axes; ++a) {
+            int d = x.in_axes[a];
+            if (d < 0 || d >= x.n_dims || (seen >> d & 1u)) { err = fmt("node %lld: bad input axis %lld", v, a); return PASE_ERR_INVALID; }
+            seen |= 1u << d;
+        }
         if (x.n_halo < 0 || x.n_halo > PASE_MAX_HALO) { err = fmt("node %lld: bad n_halo", v); return PASE_ERR_INVALID; }
-        for (int q = 0; q < x.n_halo; ++q)
+        for (int q = 0; q < x.n_halo; ++q) {
             if (x.halo_spatial[q] < 0 || x.halo_spatial[q] >= x.n_dims || x.halo_filter[q] < 0 ||
                 x.halo_filter[q] >= x.n_dims) { err = fmt("node %lld: bad halo pair %lld", v, q); return PASE_ERR_INVALID; }
+            if (!(seen >> x.halo_spatial[q] & 1u)) {        // reading L: the halo face is the input's
+                err = fmt("node %lld: halo pair %lld: spatial dim %lld is not an input-tensor axis", v, q, x.halo_spatial[q]);
+                return PASE_ERR_INVALID;
+            }
+        }
         if (x.elem_bytes < 1 || x.flops_per_point < 0) { err = fmt("node %lld: bad elem_bytes / flops", v); return PASE_ERR_INVALID; }
         if (x.flop_dims_mask >> x.n_dims) { err = fmt("node %lld: flop_dims_mask names missing dims", v); return PASE_ERR_INVALID; }
     }
@@ -223,6 +235,10 @@ pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* mach,
     P.p = p;
     P.policy = mach->cfg_policy;
     P.r = mach->flops_per_device / mach->link_bandwidth;    // r = F/B, once, fp64
+    if (!std::isfinite(P.r) || !std::isfinite(mach->flops_per_device)) {
+        err = "F must be finite and r = F/B finite (B may be +inf: r = 0)";
+        return PASE_ERR_INVALID;
+    }
     P.nodes.assign(g->nodes, g->nodes + P.n);
     P.edges.assign(g->edges, g->edges + P.m);
     for (pase_edge& e : P.edges)                            // canonicalise unused map slots

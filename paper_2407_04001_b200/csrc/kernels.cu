@@ -72,6 +72,10 @@ __device__ double d_layer_cost(const pase_node& x, const int32_t* __restrict__ c
     const int64_t out_bytes = (int64_t)x.elem_bytes * out_elems;
     const int64_t w_bytes = x.n_w_axes > 0 ? (int64_t)x.elem_bytes * w_elems : 0;
     if (x.n_w_axes == 0) g_grad = 1;
+    // conv halo (DESIGN reading L): (size_f - 1) input rows of the face of the INPUT-tensor
+    // shard across h, i.e. the input axes other than h
+    uint32_t in_m = 0;
+    for (int a = 0; a < x.n_in_axes; ++a) in_m |= 1u << x.in_axes[a];
     int64_t halo = 0;
     for (int q = 0; q < x.n_halo; ++q) {
         const int h = x.halo_spatial[q], f = x.halo_filter[q];
@@ -80,7 +84,7 @@ __device__ double d_layer_cost(const pase_node& x, const int32_t* __restrict__ c
 #pragma unroll
         for (int k = 0; k < kMaxDims; ++k) {
             if (k == h) ch = cc[k];
-            if ((out_m >> k & 1u) && k != h) face *= s[k];
+            if ((in_m >> k & 1u) && k != h) face *= s[k];
         }
         if (ch > 1 && x.size[f] > 1) halo += 2 * (int64_t)x.elem_bytes * (x.size[f] - 1) * face;
     }
@@ -921,13 +925,17 @@ __device__ __forceinline__ int ld_relaxed_sys(const int32_t* p) {
 __device__ __forceinline__ void red_add_release_sys(int32_t* p, int v) {
     asm volatile("red.release.sys.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-constexpr uint64_t kSpinTimeoutNs = 4000000000ull;    // a wait this long is reported, not hung
+// a scheduler / group-barrier wait longer than the context's timeout (PASE_SPIN_TIMEOUT_MS,
+// default 4 s; 0 = none) is reported through *err instead of hanging the GPU
+__device__ __forceinline__ bool timed_out(uint64_t t0, uint64_t limit_ns) {
+    return limit_ns != 0 && globaltimer() - t0 > limit_ns;
+}
 
 __global__ void __launch_bounds__(256, 2)
 dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ tds,
               const TaskDesc* __restrict__ tasks, const int32_t* __restrict__ order, int ntasks,
               int32_t* __restrict__ sched, int32_t* __restrict__ err, Peers peers, CostArgs cost,
-              int64_t* __restrict__ trace) {
+              int64_t* __restrict__ trace, uint64_t timeout_ns) {
     // sched: [0] claim counter (own 128-B line), [kSchedLine, +n) pending per vertex
     int32_t* head = sched;
     int32_t* pending = sched + kSchedLine;
@@ -940,6 +948,9 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
     __shared__ CostSmem csm;                                // cost-table tasks
     const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     int cur = -1;
+    // a group barrier that timed out (or any earlier failure of this solve) skips the DP: the
+    // peers' tables may still be in use (the back-substitution skips its lookups too)
+    if (ld_relaxed(err) != 0) return;
     for (;;) {
         int64_t t_claim = 0, t_start = 0;
         if (threadIdx.x == 0) {
@@ -987,7 +998,7 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
                         __nanosleep(bo);
                         bo = bo < 256 ? 2 * bo : 256;
                     }
-                    if (globaltimer() - t0 > kSpinTimeoutNs) { atomicExch(err, 1); s_task = -1; break; }
+                    if (timed_out(t0, timeout_ns)) { atomicExch(err, 1); s_task = -1; break; }
                 }
             }
             if (multi) (void)ld_acquire_sys(pv);
@@ -1034,16 +1045,16 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
 void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, const TaskDesc* tasks_dev,
                           const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
                           const Peers& peers, const CostArgs& cost, int nblocks, int64_t* trace_dev,
-                          void* stream) {
+                          uint64_t timeout_ns, void* stream) {
     dp_persistent<<<(unsigned)nblocks, 256, 0, (cudaStream_t)stream>>>(vd_dev, td_dev, tasks_dev, order_dev,
                                                                          ntasks, sched_dev, err_dev, peers,
-                                                                         cost, trace_dev);
+                                                                         cost, trace_dev, timeout_ns);
 }
 
 // Group barrier between the ranks of a multi-GPU search (before and after the DP): every
 // rank adds 1 to every rank's arrival counter (release.sys, peer atomics) and waits for
 // epoch * world arrivals on its own.  bar[0] = arrivals, bar[kSchedLine] = local epoch.
-__global__ void rank_barrier(Peers peers, int32_t* bar, int32_t* err) {
+__global__ void rank_barrier(Peers peers, int32_t* bar, int32_t* err, uint64_t timeout_ns) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const int e = bar[kSchedLine] + 1;
     bar[kSchedLine] = e;
@@ -1051,12 +1062,12 @@ __global__ void rank_barrier(Peers peers, int32_t* bar, int32_t* err) {
     const uint64_t t0 = globaltimer();
     while (ld_acquire_sys(bar) < e * peers.world) {
         __nanosleep(128);
-        if (globaltimer() - t0 > kSpinTimeoutNs) { atomicExch(err, 2); break; }
+        if (timed_out(t0, timeout_ns)) { atomicExch(err, 2); break; }
     }
 }
 
-void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev, void* stream) {
-    rank_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(peers, bar_dev, err_dev);
+void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev, uint64_t timeout_ns, void* stream) {
+    rank_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(peers, bar_dev, err_dev, timeout_ns);
 }
 
 int persistent_blocks_per_sm() {
@@ -1075,7 +1086,7 @@ template <bool SMEM>
 __global__ void __launch_bounds__(256)
 backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt_off_g, int nlev, int n,
                  const double* __restrict__ root_T, int32_t* __restrict__ choice, double* __restrict__ total,
-                 const int32_t* __restrict__ err, char* __restrict__ host_out) {
+                 int32_t* __restrict__ err, char* __restrict__ host_out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // SMEM: records and level offsets staged once (coalesced), choices kept on chip; only the
     // A(i) reads of the dependent chain go to memory (L2-resident: the DP has just written them)
@@ -1094,6 +1105,9 @@ backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt
         __syncthreads();
     }
     // a DP that reported an error (scheduler time-out) left tables unfinished: no lookups
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
     const int failed = *err;
     for (int lev = 0; lev < (failed ? 0 : nlev); ++lev) {
         for (int k = bt_off[lev] + threadIdx.x; k < bt_off[lev + 1]; k += blockDim.x) {
@@ -1103,10 +1117,14 @@ backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt
                 idx += (int64_t)ch[d.dep[a]] * stride;
                 stride *= d.radix[a];
             }
-            ch[d.node] = d.A[idx];
+            int c = d.A[idx];
+            if (c >= d.K) { s_bad = 1; c = 0; }           // no finite candidate: report, stay in range
+            ch[d.node] = c;
         }
         __syncthreads();
     }
+    if (s_bad && threadIdx.x == 0) *err = 3;
+    __syncthreads();
     // results: the device block (total | err | pad | choice[n]) and, when given, the same
     // layout straight into the caller's pinned host block (mapped: no copy-engine round trip)
     int32_t* hc = host_out ? reinterpret_cast<int32_t*>(host_out + 16) : nullptr;
@@ -1126,7 +1144,7 @@ backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt
 }
 
 void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,
-                      const double* root_T, int32_t* choice_dev, double* total_dev, const int32_t* err_dev,
+                      const double* root_T, int32_t* choice_dev, double* total_dev, int32_t* err_dev,
                       void* host_out, void* stream) {
     const size_t smem = (sizeof(BtDesc) + sizeof(int32_t)) * (size_t)n + sizeof(int32_t) * (size_t)(nlev + 1);
     if (smem <= 48 * 1024)

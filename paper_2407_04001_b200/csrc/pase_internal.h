@@ -207,6 +207,7 @@ struct CostSmem {            // its shared memory ([axis][config]: conflict-free
 struct BtDesc {               // back-substitution record of one rank, in back-level order
     const uint16_t* A;       // argmin table A(i)
     int32_t node;            // sigma_i
+    int32_t K;               // |C(sigma_i)|: a stored argmin >= K means no finite candidate
     int32_t m;               // |D(i)|
     int32_t dep[kMaxDep];    // D(i) node ids, ascending rank
     int32_t radix[kMaxDep];
@@ -226,11 +227,11 @@ void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vert
 void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, const TaskDesc* tasks_dev,
                           const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
                           const Peers& peers, const CostArgs& cost, int nblocks, int64_t* trace_dev,
-                          void* stream);
-void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev, void* stream);
+                          uint64_t timeout_ns, void* stream);
+void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev, uint64_t timeout_ns, void* stream);
 int persistent_blocks_per_sm();
 void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,
-                      const double* root_T, int32_t* choice_dev, double* total_dev, const int32_t* err_dev,
+                      const double* root_T, int32_t* choice_dev, double* total_dev, int32_t* err_dev,
                       void* host_out, void* stream);
 
 // assign.cpp (row f3): greedy device assignment of a strategy (DESIGN reading U)

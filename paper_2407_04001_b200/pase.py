@@ -43,6 +43,8 @@ class pase_node(C.Structure):
         ("halo_spatial", C.c_int32 * PASE_MAX_HALO),
         ("halo_filter", C.c_int32 * PASE_MAX_HALO),
         ("elem_bytes", C.c_int32),
+        ("n_in_axes", C.c_int32),
+        ("in_axes", C.c_int32 * PASE_MAX_DIMS),
     ]
 
 
@@ -173,6 +175,7 @@ def marshal_graph(graph: dict):
         w = nd.get("w_axes") or []
         fd = nd.get("flop_dims")
         halo = nd.get("halo") or []
+        ins = nd.get("in_axes") or []
         if len(halo) > HL:
             raise ValueError(f"node {v}: more than {HL} halo pairs")
         mask = 0
@@ -187,13 +190,15 @@ def marshal_graph(graph: dict):
                 fmask |= 1 << k
         rows.append([nd_, *sizes, *Z8[nd_:], mask, len(oa), *oa, *Z8[len(oa):], len(w), *w, *Z8[len(w):],
                      fmask, nd.get("flops_per_point", 2), len(halo), *[h for h, _ in halo], *Z4[len(halo):],
-                     *[f for _, f in halo], *Z4[len(halo):], nd.get("elem_bytes", 4)])
+                     *[f for _, f in halo], *Z4[len(halo):], nd.get("elem_bytes", 4),
+                     len(ins), *ins, *Z8[len(ins):]])
     if n:
         M = np.array(rows, dtype=np.int64)
         c = 0
         for k, width in (("n_dims", 1), ("size", D), ("splittable_mask", 1), ("n_out_axes", 1), ("out_axes", D),
                          ("n_w_axes", 1), ("w_axes", D), ("flop_dims_mask", 1), ("flops_per_point", 1),
-                         ("n_halo", 1), ("halo_spatial", HL), ("halo_filter", HL), ("elem_bytes", 1)):
+                         ("n_halo", 1), ("halo_spatial", HL), ("halo_filter", HL), ("elem_bytes", 1),
+                         ("n_in_axes", 1), ("in_axes", D)):
             NA[k] = M[:, c] if width == 1 else M[:, c:c + width]
             c += width
     EA = np.zeros(max(m, 1), dtype=np.dtype(pase_edge))

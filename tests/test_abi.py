@@ -135,6 +135,17 @@ def test_invalid_inputs_fail_loudly(lib):
     with pytest.raises(pase.PaseError) as ei:
         pase.Context(g, 4, device=-1)
     assert ei.value.status == 1 and "edge 0" in str(ei.value)
+    # reading L: a halo along a dim that is not an input-tensor axis
+    g = zoo.alexnet()
+    g["nodes"][0]["in_axes"] = [0, 1]                 # conv1 without h, w
+    with pytest.raises(pase.PaseError) as ei:
+        pase.Context(g, 8, device=-1)
+    assert ei.value.status == 1 and "node 0" in str(ei.value) and "input-tensor axis" in str(ei.value)
+    assert O.validate(g) == 1                         # the oracle rejects it too
+    # r = F/B must be finite (F = inf would make 0 * inf = NaN costs)
+    with pytest.raises(pase.PaseError) as ei:
+        pase.Context(zoo.mlp(), 4, device=-1, flops=float("inf"))
+    assert ei.value.status == 1
 
 
 def test_solve_needs_device(lib):
