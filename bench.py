@@ -42,7 +42,7 @@ WORKLOADS = {
     "chain200": ("chain200", 4, "exact_p", "latency probe: 200-GEMM path, p=4 (not a paper config)"),
 }
 SM_COUNT = 148
-FP64_LANES_PER_SM = 64          # B200 fp64 pipe, 37 TFLOP/s (FMA=2) / 148 SM / 1.965 GHz / 2
+FP64_LANES_PER_SM = 64          # fallback only: 148 SM x 64 fp64 lanes x clock
 
 
 def env_int(k, d):
@@ -101,6 +101,21 @@ def load_peaks():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return {}
+
+
+def fp64_peaks(sm_mhz):
+    """The ALU ceilings of the DP fill, MEASURED on this pool's B200 by scripts/fp64_peak.cu
+    (profiles/fp64_peak.json): DADD instructions/s of independent chains, and the DP's
+    candidate step (DADD + DSETP + argmin selects on registers) per second.  Falls back to the
+    unit-count derivation (148 SM x 64 fp64 lanes x clock) only if the file is missing."""
+    try:
+        f = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        return (f["dadd_per_s"] / 1e12, f["candidates_per_s"],
+                f"measured: profiles/fp64_peak.json (scripts/fp64_peak.cu, {f['when']}, "
+                f"SM {f['clocks']['sm_mhz']:.0f} MHz)")
+    except Exception:
+        return (SM_COUNT * FP64_LANES_PER_SM * sm_mhz * 1e6 / 1e12, None,
+                f"derived (fallback): {SM_COUNT} SM x {FP64_LANES_PER_SM} fp64 lanes x {sm_mhz:.0f} MHz")
 
 
 def oracle_solve(graph, p, policy, threads):
@@ -314,7 +329,7 @@ def main():
     peaks = load_peaks()
     clocks = clk.summary()
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
-    fp64_peak = SM_COUNT * FP64_LANES_PER_SM * sm_mhz * 1e6 / 1e12          # Tops/s
+    fp64_peak, cand_peak, peak_source = fp64_peaks(sm_mhz)                  # Tops/s, candidates/s
     mean_dp = statistics.mean(dp_ms)
     achieved = st["dp_fp64_ops"] / (mean_dp / 1e3) / 1e12
     hbm_peak = peaks.get("hbm_gbs", 6538.0)
@@ -333,7 +348,11 @@ def main():
     if alt is not None:
         a_ach = alt["dp_fp64_ops"] / (alt["dp_fill_ms"] / 1e3) / 1e12
         alt["roofline"] = {"bound": "alu", "achieved": a_ach, "peak": fp64_peak, "unit": "TFLOP/s",
-                           "frac": a_ach / fp64_peak}
+                           "frac": a_ach / fp64_peak, "peak_source": peak_source}
+        if cand_peak:
+            c_ach = alt["candidates"] / (alt["dp_fill_ms"] / 1e3)
+            alt["roofline"]["candidate_view"] = {"achieved": c_ach, "peak": cand_peak, "unit": "candidates/s",
+                                                 "frac": c_ach / cand_peak}
     line = {
         "metric": "DP entries/s (strategy search, PaSE Eq. 4 / Fig. 5)",
         "value": value, "unit": "entries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -349,7 +368,10 @@ def main():
         "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
                      "kernel": "dp_persistent (the whole DP phase is one persistent launch; timed by CUDA event nodes in the solve graph)",
-                     "peak_source": f"derived: {SM_COUNT} SM x {FP64_LANES_PER_SM} fp64 lanes x {sm_mhz:.0f} MHz (DESIGN §5)",
+                     "peak_source": peak_source,
+                     "what": "algorithmic fp64 ops (per candidate: terms-1 adds + 1 compare) / DP time vs measured DADD/s",
+                     "candidate_view": ({"achieved": cand / (mean_dp / 1e3), "peak": cand_peak, "unit": "candidates/s",
+                                         "frac": cand / (mean_dp / 1e3) / cand_peak} if cand_peak else None),
                      "hbm_view": {"achieved_gbs": hbm_achieved, "peak_gbs": hbm_peak,
                                   "frac": hbm_achieved / hbm_peak, "alg_bytes": int(st["alg_bytes_dp"])}},
         "cpu_baseline": cpu,

@@ -546,12 +546,43 @@ def random_model_graph(n: int, seed: int, extra_p: float = 0.3, max_log: int = 4
     return g.graph()
 
 
+# ----------------------------------------------------------------------------
+# Synthetic streaming-regime benchmark ("add a synthetic streaming
+# benchmark: a chain whose child table spans D ∪ {σ}"); NOT a paper config.
+# ----------------------------------------------------------------------------
+def streaming_clique(extra: int = 3, batch: int = 64, seq: int = 256, heads: int = 16,
+                     head_dim: int = 64, d_model: int = 1024) -> dict:
+    """A clique of 2 + `extra` projection-shaped vertices (b, s, h, c, d: the Transformer's q/k/v
+    shape, K = 205 at p = 64 under EXACT_P).  Vertex 0 has no splittable dim (K = 1), so SortNodes
+    eliminates it first with D = all others: its table spans (sigma_1, D(1)) -- 205^(extra+1)
+    entries (extra = 3: 1.77e9 entries, 14 GB) -- and vertex 1, eliminated next with
+    D(1) = {2..}, reads each entry of it exactly once (one 8-B read per candidate, nothing reused):
+    the streaming regime, where the DP fill is HBM-bound."""
+    g = GraphBuilder()
+    dims = [("b", batch), ("s", seq), ("h", heads), ("c", head_dim), ("d", d_model)]
+    n = 2 + extra
+    for i in range(n):
+        g.node(f"x{i}", "qkv_proj", dims, out=["b", "s", "h", "c"], w=["h", "c", "d"], fpp=6,
+               unsplittable=("b", "s", "h", "c", "d") if i == 0 else ())
+    for a in range(n):
+        for c in range(a + 1, n):
+            g.edge(a, c)
+    return g.graph()
+
+
 BENCH_GRAPHS = {
     "mlp": (mlp, 4),
     "alexnet": (alexnet, 8),
     "inception_v3": (inception_v3, 32),
     "rnnlm": (rnnlm_unrolled, 64),
     "gnmt": (gnmt_unrolled, 64),
+    # GNMT at 4 + 4 layers (SURVEY §8.d.1 row 4b, sizing rule iii): M = 5, 7.2e10 candidates,
+    # 2.6e9 table entries (26 GB of T + A): the paper-shaped config where tables leave L2
+    "gnmt4": (lambda: gnmt_unrolled(layers=4), 64),
+    # real GNMT depth (8 + 8): M = 15 > PASE_MAX_DEP -> PASE_ERR_RESOURCE (Table 1's "OOM" analogue)
+    "gnmt8": (lambda: gnmt_unrolled(layers=8), 64),
+    # synthetic streaming-regime benchmark (not a paper config): 14 GB child table read once
+    "stream205": (streaming_clique, 64),
     "transformer": (transformer, 64),
     # latency microbenchmark (not a paper config): a 200-vertex path, |D(i)| = 1, K = 6
     "chain200": (lambda: mlp(layers=200), 4),
