@@ -36,6 +36,8 @@ WORKLOADS = {
     "inception_v3": ("inception_v3", 32, "exact_p", "InceptionV3 218 vertices, b128, p=32, EXACT_P"),
     "gnmt": ("gnmt", 64, "exact_p", "GNMT unrolled 2+2 layers x 40 steps, p=64, EXACT_P"),
     "gnmt_le": ("gnmt", 64, "le_p", "GNMT unrolled 2+2 layers x 40 steps, p=64, LE_P"),
+    "gnmt4": ("gnmt4", 64, "exact_p", "GNMT unrolled 4+4 layers x 40 steps, p=64, EXACT_P (M=5, 2.6e9 table entries)"),
+    "stream205": ("stream205", 64, "exact_p", "SYNTHETIC streaming-regime clique (not a paper config): 14 GB child table read once, p=64, EXACT_P"),
     "rnnlm": ("rnnlm", 64, "exact_p", "RNNLM unrolled 2 layers x 40 steps, p=64, EXACT_P"),
     "alexnet": ("alexnet", 8, "exact_p", "AlexNet b128, p=8, EXACT_P"),
     "mlp": ("mlp", 4, "exact_p", "4-layer MLP b64 h256, p=4, EXACT_P"),

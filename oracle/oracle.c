@@ -541,9 +541,10 @@ static double w_lookup(const int64_t* edges, const int32_t* K, const double* W, 
     return W[woff[e] + (int64_t)assign[s] * K[t] + assign[t]];
 }
 
-int or_dp(int n, int m, const int64_t* edges, const int32_t* K, const double* L, const double* W,
-          int order, int threads, int64_t table_limit, int32_t* strategy, double* total,
-          double* tbl_out, int32_t* arg_out)
+/* Fig. 5 run to completion; *tbl_p / *cfg_p / *plan_p stay owned by the caller. */
+static int dp_run(int n, int m, const int64_t* edges, const int32_t* K, const double* L, const double* W,
+                  int order, int threads, int64_t table_limit, int32_t* strategy, double* total,
+                  double** tbl_p, int32_t** cfg_p, plan_t* plan_p)
 {
     plan_t P;
     if (build_plan(n, m, edges, K, order, &P)) { plan_free(&P); return 1; }
@@ -607,9 +608,47 @@ int or_dp(int n, int m, const int64_t* edges, const int32_t* K, const double* L,
         assign[v] = cfg[P.toff[i] + table_index(&P, i, K, assign)];
     }
     for (int v = 0; v < n; ++v) strategy[v] = assign[v];
+    free(assign); free(woff); free(loff);
+    *tbl_p = tbl;
+    *cfg_p = cfg;
+    *plan_p = P;
+    return 0;
+}
+
+int or_dp(int n, int m, const int64_t* edges, const int32_t* K, const double* L, const double* W,
+          int order, int threads, int64_t table_limit, int32_t* strategy, double* total,
+          double* tbl_out, int32_t* arg_out)
+{
+    double* tbl;
+    int32_t* cfg;
+    plan_t P;
+    int rc = dp_run(n, m, edges, K, L, W, order, threads, table_limit, strategy, total, &tbl, &cfg, &P);
+    if (rc) return rc;
     if (tbl_out) memcpy(tbl_out, tbl, sizeof(double) * (size_t)P.toff[n]);
     if (arg_out) memcpy(arg_out, cfg, sizeof(int32_t) * (size_t)P.toff[n]);
-    free(assign); free(cfg); free(tbl); free(woff); free(loff);
+    free(cfg); free(tbl);
+    plan_free(&P);
+    return 0;
+}
+
+int or_dp_select(int n, int m, const int64_t* edges, const int32_t* K, const double* L, const double* W,
+                 int order, int threads, int32_t* strategy, double* total,
+                 int nsel, const int32_t* sel, double* tbl_out, int32_t* arg_out)
+{
+    double* tbl;
+    int32_t* cfg;
+    plan_t P;
+    int rc = dp_run(n, m, edges, K, L, W, order, threads, 0, strategy, total, &tbl, &cfg, &P);
+    if (rc) return rc;
+    int64_t o = 0;
+    for (int k = 0; k < nsel; ++k) {
+        const int i = sel[k];
+        const int64_t sz = P.toff[i + 1] - P.toff[i];
+        memcpy(tbl_out + o, tbl + P.toff[i], sizeof(double) * (size_t)sz);
+        memcpy(arg_out + o, cfg + P.toff[i], sizeof(int32_t) * (size_t)sz);
+        o += sz;
+    }
+    free(cfg); free(tbl);
     plan_free(&P);
     return 0;
 }

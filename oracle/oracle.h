@@ -75,6 +75,12 @@ int or_dp(int n, int m, const int64_t* edges, const int32_t* K, const double* L,
           int order, int threads, int64_t table_limit, int32_t* strategy, double* total,
           double* tbl_out, int32_t* arg_out);
 
+/* or_dp, copying out only the tables of the nsel ranks sel[] (concatenated in that order) --
+ * full-size parity checks of configs whose complete tables do not fit twice in host memory. */
+int or_dp_select(int n, int m, const int64_t* edges, const int32_t* K, const double* L, const double* W,
+                 int order, int threads, int32_t* strategy, double* total,
+                 int nsel, const int32_t* sel, double* tbl_out, int32_t* arg_out);
+
 /* Eq. 2 recurrence with the BFS ordering and single predecessor table. */
 int or_dp_bfs_eq2(int n, int m, const int64_t* edges, const int32_t* K, const double* L,
                   const double* W, int64_t table_limit, int32_t* strategy, double* total);

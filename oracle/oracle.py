@@ -49,6 +49,8 @@ def lib():
             "or_sets": [C.c_int, C.c_int, i64p, i32p, C.c_int, u8p, u8p, u8p, i32p, i32p],
             "or_table_sizes": [C.c_int, C.c_int, i64p, i32p, C.c_int, i64p, i64p],
             "or_dp": [C.c_int, C.c_int, i64p, i32p, f64p, f64p, C.c_int, C.c_int, C.c_int64, i32p, f64p, f64p, i32p],
+            "or_dp_select": [C.c_int, C.c_int, i64p, i32p, f64p, f64p, C.c_int, C.c_int, i32p, f64p, C.c_int,
+                             i32p, f64p, i32p],
             "or_dp_bfs_eq2": [C.c_int, C.c_int, i64p, i32p, f64p, f64p, C.c_int64, i32p, f64p],
             "or_brute": [C.c_int, C.c_int, i64p, i32p, f64p, f64p, C.c_int64, i32p, f64p],
             "or_assign": [C.c_int, i64p, C.c_int, i64p, C.c_int, i32p, i32p, f64p],
@@ -237,6 +239,28 @@ class Problem:
         if want_tables:
             out.update(T=T, A=A, toff=off)
         return out
+
+    def dp_select(self, ranks, threads: int = 1, order: int = 0):
+        """Fig. 5 DP-Alg returning only the tables of `ranks`: dict(strategy, cost, seconds,
+        tables={rank: (T, A)})."""
+        off, _ = self.table_sizes(order)
+        ranks = [int(r) for r in ranks]
+        sizes = [int(off[r + 1] - off[r]) for r in ranks]
+        T = np.zeros(max(sum(sizes), 1), np.float64)
+        A = np.zeros(max(sum(sizes), 1), np.int32)
+        sel = np.ascontiguousarray(ranks, np.int32)
+        strat = np.zeros(self.n, np.int32)
+        tot = np.zeros(1, np.float64)
+        t0 = time.perf_counter()
+        rc = lib().or_dp_select(*self._args(), order, threads, _p(strat, C.c_int32), _p(tot, C.c_double),
+                                len(ranks), _p(sel, C.c_int32), _p(T, C.c_double), _p(A, C.c_int32))
+        dt = time.perf_counter() - t0
+        _chk(rc, "dp_select")
+        tables, o = {}, 0
+        for r, sz in zip(ranks, sizes):
+            tables[r] = (T[o:o + sz], A[o:o + sz])
+            o += sz
+        return {"strategy": strat, "cost": float(tot[0]), "seconds": dt, "tables": tables}
 
     def dp_bfs_eq2(self, table_limit: int = 0):
         strat = np.zeros(self.n, np.int32)
