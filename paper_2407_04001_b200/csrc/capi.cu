@@ -284,7 +284,7 @@ void widen_critical(pase_ctx* ctx) {
         bool changed = false;
         for (int i = 0; i < n; ++i) {
             VertexDesc& d = ctx->vd[i];
-            if (top[i] + bot[i] - w[i] < 0.85 * cp || d.shape < 0 || d.wlog != 0) continue;
+            if (top[i] + bot[i] - w[i] < 0.85 * cp || d.shape < 0 || d.shape >= pase::kShapeG1 || d.wlog != 0) continue;
             while (d.glog < 5 && (16 << d.glog) <= d.K && tasks_of(d) < nb) {
                 ++d.glog;
                 d.shape = (d.shape & ~3) | (d.glog - 2);
@@ -379,6 +379,9 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
     set_tile2(d, q2, f2);
     d.shape = pase::kShape2D + (NS - 1) * 4 + (d.glog - 2);
 }
+
+// streaming-regime vertices: spanning child tables of at least this many bytes
+const uint64_t kStreamBytes = std::getenv("PASE_STREAM_MB") ? (uint64_t)std::atoll(std::getenv("PASE_STREAM_MB")) << 20 : (64ull << 20);
 
 // latency mode: vertices with at most this many candidates (N_i * K)
 const int64_t kLatencyCand = std::getenv("PASE_LATENCY_CAND") ? std::atoll(std::getenv("PASE_LATENCY_CAND")) : (1 << 18);
@@ -563,6 +566,13 @@ pase_status prepare(pase_ctx* ctx, bool device) {
         d.ntile2 = 1;
         d.t2star = d.tstar;
         d.ostride_q2 = 0;
+        // streaming regime: a child table spanning (sigma_i, D(i)) gives every
+        // candidate one 8-B value nobody else reads; with L2-exceeding tables the vertex is
+        // HBM-bound, so full-warp lane groups read each row as 256-B coalesced segments (narrow
+        // groups would scatter a warp's loads over 8 rows: L1-wavefront bound, measured)
+        bool streaming = false;
+        for (int j : P.children[i])
+            if (P.tsize[j] == (int64_t)d.K * d.nout && (uint64_t)P.tsize[j] * 8ull >= kStreamBytes) streaming = true;
         if (!wide && NP >= 1 && NP <= 4 && NS >= 0 && NS <= 3) {
             d.glog = lane_group_log2(d.K);
             // latency mode: a small vertex (<= kLatencyCand candidates) is
@@ -579,7 +589,15 @@ pase_status prepare(pase_ctx* ctx, bool device) {
                 d.wlog = ll - d.glog;
             }
             d.shape = (NP - 1) * 16 + NS * 4 + (d.glog - 2);
-            if (d.wlog == 0 && !no_2d()) try_tile2(ctx, d, tv, top);
+            if (d.wlog == 0 && streaming) {
+                d.glog = 5;
+                d.shape = (NP - 1) * 16 + NS * 4 + 3;
+            } else if (d.wlog == 0 && d.K <= 3) {             // one lane per item
+                d.glog = 0;
+                d.shape = pase::kShapeG1 + (NP - 1) * 4 + NS;
+            } else if (d.wlog == 0 && !no_2d()) {
+                try_tile2(ctx, d, tv, top);
+            }
         } else {                                          // generic kernel
             d.glog = d.K <= 4 ? 2 : d.K <= 8 ? 3 : d.K <= 16 ? 4 : 5;
             d.shape = -1;
@@ -808,7 +826,7 @@ void fill_stats(pase_ctx* ctx) {
         const int v = P.sigma[i];
         const uint64_t terms = 1 + P.egt[i].size() + P.children[i].size();
         ops += (uint64_t)P.tsize[i] * (uint64_t)P.K[v] * terms;
-        b += (uint64_t)P.tsize[i] * 10u;
+        b += (uint64_t)P.tsize[i] * (P.K[v] > 1 ? 10u : 8u);     // K = 1: no argmin table
         for (int j : P.children[i]) b += (uint64_t)P.tsize[j] * 8u;
         for (int e : P.egt[i]) b += 8ull * (uint64_t)P.K[P.edges[e].src] * (uint64_t)P.K[P.edges[e].dst];
         b += 8ull * (uint64_t)P.K[v];
@@ -1268,7 +1286,8 @@ pase_status pase_get_dp_table(const pase_ctx* ctx_c, int32_t rank, double* T_out
     CUDA_TRY(cudaSetDevice(ctx->dev));
     const int64_t sz = ctx->P.tsize[rank], off = ctx->P.toff[rank];
     if (T_out) CUDA_TRY(cudaMemcpyAsync(T_out, ctx->d_T + off, sizeof(double) * sz, cudaMemcpyDeviceToHost, ctx->stream));
-    if (A_out) CUDA_TRY(cudaMemcpyAsync(A_out, ctx->d_A + off, sizeof(uint16_t) * sz, cudaMemcpyDeviceToHost, ctx->stream));
+    if (A_out && ctx->vd[rank].K == 1) std::memset(A_out, 0, sizeof(uint16_t) * sz);   // not stored
+    else if (A_out) CUDA_TRY(cudaMemcpyAsync(A_out, ctx->d_A + off, sizeof(uint16_t) * sz, cudaMemcpyDeviceToHost, ctx->stream));
     // multi-GPU: a partitioned table whose T is not broadcast holds only this rank's slice
     // (configs [q K/G, (q+1) K/G) of its top coordinate, the slowest): gather the others'
     // slices from their pools through the peer mappings (argmin tables are always complete)

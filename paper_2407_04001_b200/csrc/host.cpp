@@ -4,6 +4,8 @@
 //   a4 elimination tree (children(i) = {j : min-rank D(j) = i}) and layouts.
 // Written independently of oracle/ (bitset d-sets, tree rule instead of dfs).
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <map>
 #include <cmath>
 #include <cstdio>
@@ -223,6 +225,8 @@ void sort_nodes(int n, const std::vector<pase_edge>& edges, std::vector<int32_t>
 
 pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* mach, Plan& P,
                        std::string& err) {
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     if (p < 1 || p > 4096) { err = fmt("p = %lld out of range [1, 4096]", p); return PASE_ERR_INVALID; }
     if (!mach) { err = "machine is NULL"; return PASE_ERR_INVALID; }
     if (mach->cfg_policy != PASE_CFG_EXACT_P && mach->cfg_policy != PASE_CFG_LE_P) { err = "bad cfg_policy"; return PASE_ERR_INVALID; }
@@ -245,6 +249,7 @@ pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* mach,
         for (int a = P.nodes[e.src].n_out_axes; a < kMaxDims; ++a) e.axis_map[a] = -1;
     const int n = P.n, m = P.m;
 
+    const auto ta = clk::now();
     // a2
     P.K.assign(n, 0);
     P.cfg_off.assign(n + 1, 0);
@@ -271,6 +276,7 @@ pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* mach,
     }
     P.max_k = *std::max_element(P.K.begin(), P.K.end());
 
+    const auto tb = clk::now();
     // a3
     std::vector<std::vector<int32_t>> dn;
     if (mach->ordering == PASE_ORDER_BFS) sort_nodes(n, P.edges, P.sigma, dn, bfs_order(n, P.edges));
@@ -292,6 +298,7 @@ pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* mach,
         return PASE_ERR_RESOURCE;
     }
 
+    const auto tc = clk::now();
     // a4: elimination tree, E>(sigma_i), levels
     P.parent.assign(n, -1);
     P.children.assign(n, {});
@@ -332,6 +339,7 @@ pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* mach,
         P.levels = std::max(P.levels, lv + 1);
     }
 
+    const auto td = clk::now();
     // layouts
     P.tsize.assign(n, 1);
     P.toff.assign(n + 1, 0);
@@ -364,6 +372,11 @@ pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* mach,
     P.woff.assign(m + 1, 0);
     for (int e = 0; e < m; ++e)
         P.woff[e + 1] = P.woff[e] + (int64_t)P.K[P.edges[e].src] * P.K[P.edges[e].dst];
+    if (const char* tv = std::getenv("PASE_TIMING"); tv && tv[0] == '1') {
+        auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "[pase] plan: ingest %.3f ms, C(v) %.3f ms, SortNodes %.3f ms, tree %.3f ms, layout %.3f ms\n",
+                     ms(t0, ta), ms(ta, tb), ms(tb, tc), ms(tc, td), ms(td, clk::now()));
+    }
     return PASE_OK;
 }
 

@@ -262,13 +262,16 @@ __device__ __forceinline__ void st_u16(uint16_t* p, int c) {
 }
 // Output of one DP entry; multi-GPU broadcast vertices also write it into every peer's copy
 // of the table (peer stores over NVLink: the all-gather fused into the producer).
+// A vertex with a single configuration (K = 1) has no argmin to record: its A(i) is never
+// written (the back-substitution knows the choice is 0).
 __device__ __forceinline__ void st_out(const VertexDesc& vd, int64_t phi, double v, int c) {
     st_f64(vd.T + phi, v);
-    st_u16(vd.A + phi, c);
+    const bool arg = vd.K > 1;
+    if (arg) st_u16(vd.A + phi, c);
     if (vd.bcast)
         for (int q = 0; q < vd.npeer; ++q) {
             if (vd.bcast & 1) st_f64(vd.Tpeer[q] + phi, v);
-            st_u16(vd.Apeer[q] + phi, c);
+            if (arg) st_u16(vd.Apeer[q] + phi, c);
         }
 }
 
@@ -814,6 +817,16 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
 #undef PASE_NP
 #undef PASE_NS
 #undef PASE_CASE
+        // one lane per item (K <= 3): the whole reduction over C in one thread, 8 outputs per
+        // thread, consecutive threads on consecutive items -- every store is a coalesced warp row
+#define PASE_CASE1(NP, NS)                                                                        \
+    case kShapeG1 + (NP - 1) * 4 + NS:                                                            \
+        tile_items<NP, NS, 1>(vd, td_sh, i0 + first_warp * 32, nwarps * 32, i1, red_b, red_c);    \
+        return;
+#define PASE_NP1(NP) PASE_CASE1(NP, 0) PASE_CASE1(NP, 1) PASE_CASE1(NP, 2) PASE_CASE1(NP, 3)
+        PASE_NP1(1) PASE_NP1(2) PASE_NP1(3) PASE_NP1(4)
+#undef PASE_NP1
+#undef PASE_CASE1
 #define PASE_CASE2(NS, LGG)                                                                       \
     case kShape2D + (NS - 1) * 4 + (LGG - 2): {                                                   \
         constexpr int G_ = 1 << LGG, GPW_ = 32 / G_;                                              \
@@ -1117,7 +1130,7 @@ backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt
                 idx += (int64_t)ch[d.dep[a]] * stride;
                 stride *= d.radix[a];
             }
-            int c = d.A[idx];
+            int c = d.K > 1 ? d.A[idx] : 0;                // K = 1: A(i) is not stored
             if (c >= d.K) { s_bad = 1; c = 0; }           // no finite candidate: report, stay in range
             ch[d.node] = c;
         }

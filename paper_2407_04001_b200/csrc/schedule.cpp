@@ -74,7 +74,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
             // instead of K/G.  Same items, same results.
             int64_t bulk_end = -1;
             int32_t tail_glog = 0;
-            if (kWaveTail && runs.size() == 1 && d.shape >= 0 && d.wlog == 0 && d.glog < 5 && ti == groups) {
+            if (kWaveTail && runs.size() == 1 && d.shape >= 0 && d.shape < kShapeG1 && d.wlog == 0 && d.glog < 5 && ti == groups) {
                 const int64_t T = (local + ti - 1) / ti;
                 if (T > nblocks && T % nblocks != 0) {
                     const int64_t bulk = (T / nblocks) * nblocks * ti;
@@ -139,7 +139,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     for (int64_t t = 0; t < ntk; ++t) {
         if (all[t].vtx >= n) { tdur[t] = 4.0; continue; }  // a cost-table chunk
         const VertexDesc& d = vd[all[t].vtx];
-        const double cand = (double)(all[t].i1 - all[t].i0) * d.K * (d.shape < 0 ? 1 : d.q2 >= 0 ? kTile1 * kTile2 : kTile);
+        const double cand = (double)(all[t].i1 - all[t].i0) * d.K * (d.shape < 0 ? 1 : d.q2 >= 0 ? kTile1 * kTile2 : kTile);  // G1 items: kTile outputs too
         const double lanes = all[t].glog ? (double)(1 << (all[t].glog - d.glog)) : 1.0;   // wave tail
         tdur[t] = 3.0 + cand / (3000.0 * lanes);
     }

@@ -208,3 +208,32 @@ def test_premarshalled_graph_same_plan(lib):
         assert np.array_equal(a.K(), b.K())
         b.close()
     a.close()
+
+
+def test_gnmt_depth_guard(lib):
+    """SURVEY §8.d.1 row 4b / sizing rule iii: GNMT 4+4 plans (M = 5, the same candidate count
+    as the oracle's Fig. 5 plan); the real 8+8 depth trips the width guard (M = 15 > 12,
+    PASE_ERR_RESOURCE naming M and K) -- the BF-'OOM' analogue of Table 1."""
+    g, p = zoo.bench_graph("gnmt4")
+    ctx = pase.Context(g, p, device=-1)
+    st = ctx.stats()
+    assert st["max_dep"] == 5 and st["max_configs"] == 28
+    K = ctx.K()
+    P = O.Problem(g, K, [np.zeros(k) for k in K], [np.zeros((K[e["src"]], K[e["dst"]])) for e in g["edges"]])
+    assert P.table_sizes()[1] == st["candidates"]
+    g8, p8 = zoo.bench_graph("gnmt8")
+    with pytest.raises(pase.PaseError) as ei:
+        pase.Context(g8, p8, device=-1)
+    assert ei.value.status == 2 and "M = max |D(i)| = 15" in str(ei.value) and "K = 28" in str(ei.value)
+
+
+def test_streaming_clique_plan(lib):
+    """The synthetic streaming benchmark's structure: vertex 0 (K = 1) first with D = the rest,
+    vertex 1 next with D(1) = D(0) - {1}: T(0) spans (sigma_1, D(1)) -- 205^4 entries."""
+    g, p = zoo.bench_graph("stream205")
+    ctx = pase.Context(g, p, device=-1)
+    sigma, deps, parent = ctx.order()
+    K = ctx.K()
+    assert list(sigma[:2]) == [0, 1] and K[0] == 1 and all(k == 205 for k in K[1:])
+    assert deps[0] == [1, 2, 3, 4] and deps[1] == [2, 3, 4] and parent[0] == 1
+    assert ctx.stats()["table_entries"] > 205 ** 4
