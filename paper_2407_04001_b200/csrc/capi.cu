@@ -18,6 +18,14 @@
 #include <vector>
 
 #include "pase_internal.h"
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: phase ranges for nsys / ncu --nvtx (no-ops untraced)
+
+namespace {
+struct NvtxRange {               // RAII NVTX push/pop (tracing)
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 using pase::EdgeDesc;
 using pase::Plan;
@@ -469,6 +477,8 @@ pase_status allocate(pase_ctx* ctx, bool device) {
 
 // Vertex/term descriptors, the task schedule (schedule.cpp), pool 2, upload.
 pase_status prepare(pase_ctx* ctx, bool device) {
+    using clk = std::chrono::steady_clock;
+    const auto p0 = clk::now();
     const Plan& P = ctx->P;
     const int n = P.n, m = P.m;
     std::vector<EdgeDesc> ed(std::max(m, 1));
@@ -603,6 +613,7 @@ pase_status prepare(pase_ctx* ctx, bool device) {
             d.shape = -1;
         }
     }
+    const auto p1 = clk::now();
     widen_critical(ctx);
     for (VertexDesc& d : ctx->vd) {                       // partitioned item order (split_item)
         d.psub = (d.part && d.shape >= 0) ? (int32_t)(d.ncombo / d.radix[d.m - 1]) : 1;
@@ -613,6 +624,7 @@ pase_status prepare(pase_ctx* ctx, bool device) {
         pase::fastdiv_magic((uint32_t)std::max(1, d.ntile2), d.mul_tile2, d.sh_tile2);
         pase::fastdiv_magic((uint32_t)std::max(1, d.psub), d.mul_psub, d.sh_psub);
     }
+    const auto p2 = clk::now();
     // tasks, broadcast flags, pending counters, claim order (schedule.cpp)
     std::vector<int32_t> consumer(chunks.size());
     for (size_t k = 0; k < chunks.size(); ++k) consumer[k] = chunks[k].consumer;
@@ -622,6 +634,7 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     ctx->ntasks = (int)ctx->sp.tasks.size();
     ctx->total_tasks = ctx->sp.total_tasks;
     for (VertexDesc& d : ctx->vd) d.npeer = d.bcast ? ctx->world - 1 : 0;
+    const auto p3 = clk::now();
     // pool 2
     const size_t sched_words = pase::kSchedLine + (size_t)n;
     ctx->sched_bytes = sizeof(int32_t) * sched_words;
@@ -675,6 +688,11 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     const size_t size1 = (size_t)((char*)ctx->d_L - (char*)ctx->pool);
     const size_t size2 = (size_t)((char*)ctx->d_sched - (char*)ctx->pool2);
     ctx->h2d_bytes = size1 + size2;
+    if (const char* tv = std::getenv("PASE_TIMING"); tv && tv[0] == '1') {
+        auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "[pase] prepare: descriptors %.3f ms, widen %.3f ms, schedule %.3f ms, pool2+bt %.3f ms\n",
+                     ms(p0, p1), ms(p1, p2), ms(p2, p3), ms(p3, clk::now()));
+    }
     if (!device) return PASE_OK;
     char* img = (char*)stage_get(size1 + size2);
     if (!img) { ctx->err = "cudaMallocHost of the upload image failed"; return PASE_ERR_RESOURCE; }
@@ -901,7 +919,11 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
         pase_destroy(ctx);
         return code;
     };
-    pase_status st = pase::build_plan(g, p, m, ctx->P, ctx->err);
+    pase_status st;
+    {
+        NvtxRange r("pase_create/plan (a1-a4)");
+        st = pase::build_plan(g, p, m, ctx->P, ctx->err);
+    }
     if (st) return fail(st);
     const bool device = ctx->dev >= 0;
     {
@@ -977,7 +999,11 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
     auto t_plan = std::chrono::steady_clock::now();
     if ((st = allocate(ctx, true))) return fail(st);
     auto t_alloc = std::chrono::steady_clock::now();
-    if ((st = prepare(ctx, true))) return fail(st);
+    {
+        NvtxRange r("pase_create/prepare+upload");
+        st = prepare(ctx, true);
+    }
+    if (st) return fail(st);
     auto t_upload = std::chrono::steady_clock::now();
     if ((st = record_graph(ctx))) return fail(st);
     // the pools are complete before any other stream (a peer's, the legacy one used by the
@@ -1002,6 +1028,7 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
 
 pase_status pase_launch(pase_ctx* ctx) {
     if (!ctx) return PASE_ERR_INVALID;
+    NvtxRange r("pase_launch (a5-a8 enqueue)");
     if (ctx->dev < 0) { ctx->err = "host-only planning context: no solve"; return PASE_ERR_STATE; }
     if (ctx->world > 1 && !ctx->connected) { ctx->err = "multi-GPU context: call pase_connect first"; return PASE_ERR_STATE; }
     if (ctx->launched) { ctx->err = "pase_launch called twice without pase_finish"; return PASE_ERR_STATE; }
@@ -1028,6 +1055,7 @@ pase_status pase_finish(pase_ctx* ctx, int32_t* configs_out, int32_t* config_ind
     if (!ctx) return PASE_ERR_INVALID;
     if (!ctx->launched) { ctx->err = "pase_finish without pase_launch"; return PASE_ERR_STATE; }
     ctx->launched = false;
+    NvtxRange r("pase_finish (wait + strategy)");
     CUDA_TRY(cudaSetDevice(ctx->dev));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     if (*ctx->h_err) {
@@ -1221,7 +1249,10 @@ pase_status pase_get_configs(const pase_ctx* ctx, int32_t* counts, int32_t* tupl
     if (!ctx) return PASE_ERR_INVALID;
     const Plan& P = ctx->P;
     if (counts) std::copy(P.K.begin(), P.K.end(), counts);
-    if (tuples) std::copy(P.cfg.begin(), P.cfg.end(), tuples);
+    if (tuples)                                   // per node in id order (shared blocks expanded)
+        for (int v = 0, o = 0; v < P.n; o += P.K[v], ++v)
+            std::copy(P.cfg.begin() + P.cfg_off[v] * pase::kMaxDims, P.cfg.begin() + (P.cfg_off[v] + P.K[v]) * pase::kMaxDims,
+                      tuples + (size_t)o * pase::kMaxDims);
     return PASE_OK;
 }
 

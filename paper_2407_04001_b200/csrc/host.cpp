@@ -255,25 +255,27 @@ pase_status build_plan(const pase_graph* g, int32_t p, const pase_machine* mach,
     P.cfg_off.assign(n + 1, 0);
     P.cfg.clear();
     std::vector<int32_t> rows;
-    // C(v) depends only on (n_dims, size[], splittable_mask, p, policy): enumerate each
-    // distinct iteration space once (the zoo's layers repeat per block / time step)
-    std::map<std::vector<int64_t>, std::vector<int32_t>> memo;
+    // C(v) depends only on (n_dims, size[], splittable_mask, p, policy): each distinct
+    // iteration space is enumerated once and stored once (the zoo's layers repeat per block /
+    // time step); nodes of the same space share its rows (cfg_off = start of the shared block)
+    std::map<std::vector<int64_t>, std::pair<int64_t, int32_t>> memo;   // key -> (offset, K)
+    std::vector<int64_t> key;
     for (int v = 0; v < n; ++v) {
         const pase_node& x = P.nodes[v];
-        std::vector<int64_t> key(x.size, x.size + x.n_dims);
+        key.assign(x.size, x.size + x.n_dims);
         key.push_back(x.splittable_mask);
         auto it = memo.find(key);
         if (it == memo.end()) {
             enumerate(x, p, P.policy, rows);
-            it = memo.emplace(std::move(key), rows).first;
+            const int64_t k = (int64_t)rows.size() / kMaxDims;
+            if (k < 1 || k > 65535) { err = fmt("node %lld: %lld configurations (supported 1..65535)", v, k); return PASE_ERR_RESOURCE; }
+            it = memo.emplace(key, std::make_pair((int64_t)P.cfg.size() / kMaxDims, (int32_t)k)).first;
+            P.cfg.insert(P.cfg.end(), rows.begin(), rows.end());
         }
-        rows = it->second;
-        int64_t k = (int64_t)rows.size() / kMaxDims;
-        if (k < 1 || k > 65535) { err = fmt("node %lld: %lld configurations (supported 1..65535)", v, k); return PASE_ERR_RESOURCE; }
-        P.K[v] = (int32_t)k;
-        P.cfg_off[v + 1] = P.cfg_off[v] + k;
-        P.cfg.insert(P.cfg.end(), rows.begin(), rows.end());
+        P.K[v] = it->second.second;
+        P.cfg_off[v] = it->second.first;
     }
+    P.cfg_off[n] = (int64_t)P.cfg.size() / kMaxDims;          // rows in the shared pool
     P.max_k = *std::max_element(P.K.begin(), P.K.end());
 
     const auto tb = clk::now();

@@ -25,8 +25,9 @@ struct Plan {
 
     // a2: C(v) -- per node K_v and its tuples (row-major, kMaxDims int32 per config)
     std::vector<int32_t> K;
-    std::vector<int64_t> cfg_off;                // n+1, in configs
-    std::vector<int32_t> cfg;                    // cfg_off[n] * kMaxDims
+    std::vector<int64_t> cfg_off;                // n+1, in configs: start of C(v) in cfg (nodes of one
+                                                 // iteration space share a block); [n] = rows in cfg
+    std::vector<int32_t> cfg;                    // cfg_off[n] * kMaxDims (distinct spaces only)
 
     // a3: SortNodes (Fig. 4): sigma (rank -> node), rank (node -> rank), D(i) by rank
     std::vector<int32_t> sigma, rank;
