@@ -82,6 +82,7 @@ struct pase_ctx {
     int64_t total_tasks = 0;
     uint64_t timeout_ns = 4000000000ull;    // scheduler / barrier wait limit (PASE_SPIN_TIMEOUT_MS)
     bool persistent = true;
+    bool stream_tiles = false;              // some vertex uses the TMA-staged stream tile
     bool cost_tasks = false;                // persistent: cost tables as tasks of the DP kernel
     // multi-GPU
     pase::Peers peers{};
@@ -388,6 +389,11 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
     d.shape = pase::kShape2D + (NS - 1) * 4 + (d.glog - 2);
 }
 
+bool stream_tma() {
+    static const bool on = !(std::getenv("PASE_STREAM_TMA") && std::getenv("PASE_STREAM_TMA")[0] == '0');
+    return on;
+}
+
 // streaming-regime vertices: spanning child tables of at least this many bytes
 const uint64_t kStreamBytes = std::getenv("PASE_STREAM_MB") ? (uint64_t)std::atoll(std::getenv("PASE_STREAM_MB")) << 20 : (64ull << 20);
 
@@ -580,9 +586,12 @@ pase_status prepare(pase_ctx* ctx, bool device) {
         // candidate one 8-B value nobody else reads; with L2-exceeding tables the vertex is
         // HBM-bound, so full-warp lane groups read each row as 256-B coalesced segments (narrow
         // groups would scatter a warp's loads over 8 rows: L1-wavefront bound, measured)
-        bool streaming = false;
+        bool streaming = false, last_spans = false;
         for (int j : P.children[i])
-            if (P.tsize[j] == (int64_t)d.K * d.nout && (uint64_t)P.tsize[j] * 8ull >= kStreamBytes) streaming = true;
+            if (P.tsize[j] == (int64_t)d.K * d.nout && (uint64_t)P.tsize[j] * 8ull >= kStreamBytes) {
+                streaming = true;
+                last_spans = j == P.children[i].back();   // the spanning table is the last term
+            }
         if (!wide && NP >= 1 && NP <= 4 && NS >= 0 && NS <= 3) {
             d.glog = lane_group_log2(d.K);
             // latency mode: a small vertex (<= kLatencyCand candidates) is
@@ -602,6 +611,8 @@ pase_status prepare(pase_ctx* ctx, bool device) {
             if (d.wlog == 0 && streaming) {
                 d.glog = 5;
                 d.shape = (NP - 1) * 16 + NS * 4 + 3;
+                // its rows staged into shared memory by TMA bulk copies
+                if (last_spans && NS >= 1 && stream_tma()) d.shape = pase::kShapeStream + (NP - 1) * 4 + NS;
             } else if (d.wlog == 0 && d.K <= 3) {             // one lane per item
                 d.glog = 0;
                 d.shape = pase::kShapeG1 + (NP - 1) * 4 + NS;
@@ -615,6 +626,8 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     }
     const auto p1 = clk::now();
     widen_critical(ctx);
+    ctx->stream_tiles = false;
+    for (const VertexDesc& d : ctx->vd) ctx->stream_tiles = ctx->stream_tiles || d.shape >= pase::kShapeStream;
     for (VertexDesc& d : ctx->vd) {                       // partitioned item order (split_item)
         d.psub = (d.part && d.shape >= 0) ? (int32_t)(d.ncombo / d.radix[d.m - 1]) : 1;
         // magic numbers of the work-item decode (division by invariant integers)
@@ -769,7 +782,7 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
         if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, ctx->timeout_ns, s);
         pase::launch_dp_persistent(ctx->d_vd, ctx->d_td, ctx->d_tasks, ctx->d_order, ctx->ntasks, ctx->d_sched,
                                    d_err, ctx->peers, cost_args(ctx), ctx->nblocks,
-                                   trace_on() ? ctx->d_trace : nullptr, ctx->timeout_ns, s);
+                                   trace_on() ? ctx->d_trace : nullptr, ctx->timeout_ns, ctx->stream_tiles, s);
         if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, ctx->timeout_ns, s);
     } else {
         CUDA_TRY(cudaEventRecord(start, s));

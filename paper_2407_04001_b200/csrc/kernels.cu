@@ -794,12 +794,221 @@ __device__ __noinline__ void generic_items(const VertexDesc& vd, const TermDesc*
     }
 }
 
+
+// =====================================================================================
+// Streaming-regime tile: the vertex's last term is a child table
+// spanning (sigma_i, D(i)), so every candidate reads one 8-B value that nothing else reads and
+// the vertex is HBM-bound.  The rows of that term are STAGED INTO SHARED MEMORY BY TMA BULK
+// COPIES (cp.async.bulk, completion on a per-stage mbarrier) in a kStreamStages-deep ring per
+// warp over the reduction range: chunk c of an item = C in [32c, 32c + 32) of its kTile rows,
+// so (kStreamStages - 1) chunks of every warp are in flight while it reduces the current one.
+// Everything else is the 1-D tile with one item per warp (G = 32): the prefix terms [0, tstar)
+// summed once per C, the suffix terms per output, the spanning term last, strict < over
+// increasing C, butterfly argmin -- the canonical association, so results stay bit-identical.
+// =====================================================================================
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(__cvta_generic_to_global(src)), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+constexpr int kStreamStages = 4;                         // chunks per warp ring
+constexpr int kStreamRow = 34;                           // doubles per staged row chunk: 32 + alignment
+constexpr int kStreamStage = kTile * kStreamRow;         // doubles per stage (kTile rows)
+constexpr int kStreamWarps = 8;                          // warps per CTA (256 threads)
+constexpr size_t kStreamSmemBytes = (size_t)kStreamWarps * kStreamStages * kStreamStage * 8 +
+                                    (size_t)kStreamWarps * kStreamStages * 8;
+
+// ring of warp w: stages at dyn + w * stages * stage, barriers after all stages
+__device__ __forceinline__ double* stream_buf(unsigned char* dyn, int w) {
+    return reinterpret_cast<double*>(dyn) + (size_t)w * kStreamStages * kStreamStage;
+}
+__device__ __forceinline__ uint64_t* stream_bar(unsigned char* dyn, int w) {
+    return reinterpret_cast<uint64_t*>(dyn + (size_t)kStreamWarps * kStreamStages * kStreamStage * 8) + w * kStreamStages;
+}
+__device__ __forceinline__ void stream_init(unsigned char* dyn) {      // once per CTA, before any use
+    if (threadIdx.x < kStreamWarps * kStreamStages) mbar_init(stream_bar(dyn, 0) + threadIdx.x, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+}
+
+// Decode of one item for the stream tile: output base, row pointers of every term at the
+// item's combination (tiled coordinate at x0), rows in the tile.
+template <int NP, int NS>
+__device__ __forceinline__ void stream_decode(const VertexDesc& vd, const TermDesc* td, int64_t item,
+                                              int64_t& obase, const double** pp, const double** sp, int& x0,
+                                              int& nb) {
+    const int q = vd.qstar;
+    uint32_t rem, tix;
+    split_item(vd, (uint32_t)item, rem, tix);
+    x0 = (int)tix * kTile;
+    nb = min(kTile, vd.rq - x0);
+#pragma unroll
+    for (int t = 0; t < NP; ++t) pp[t] = td[t].base;
+#pragma unroll
+    for (int t = 0; t < NS; ++t) sp[t] = td[NP + t].base + (int64_t)x0 * td[NP + t].stride[q];
+    obase = 0;
+    int64_t ost = 1;
+    for (int c = 0; c < vd.m; ++c) {
+        const uint32_t r = (uint32_t)vd.radix[c];
+        if (c != q) {
+            const uint32_t qv = fdiv(rem, vd.rmul[c], vd.rsh[c]);
+            const uint32_t v = rem - qv * r;
+            rem = qv;
+            obase += (int64_t)v * ost;
+#pragma unroll
+            for (int t = 0; t < NP; ++t) pp[t] += (int64_t)v * td[t].stride[c];
+#pragma unroll
+            for (int t = 0; t < NS; ++t) sp[t] += (int64_t)v * td[NP + t].stride[c];
+        }
+        ost *= r;
+    }
+}
+
+template <int NP, int NS>
+__device__ __noinline__ uint32_t tile_stream_items(const VertexDesc& vd, const TermDesc* td, int64_t first,
+                                                   int64_t stride, int64_t end, unsigned char* dyn, uint32_t seq) {
+    constexpr int V = kTile, S = 3, H = 1;               // G = 32: 3 halving steps, then 2 more
+    const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & (kStreamWarps - 1);
+    double* buf = stream_buf(dyn, w);
+    uint64_t* bar = stream_bar(dyn, w);
+    const int q = vd.qstar;
+    const int K = vd.K;
+    const int nch = (K + 31) >> 5;
+    const int64_t sqs = td[NP + NS - 1].stride[q];       // row stride of the spanning term's tile
+    int sq[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) sq[t] = (int)td[NP + t].stride[q];
+    // producer cursor (warp-uniform): next (item, chunk) to stage; lanes < kTile hold its row
+    int64_t pitem = first;
+    int pch = 0;
+    const double* prow = nullptr;
+    auto prow_of = [&](int64_t item) {
+        int64_t ob;
+        const double* pp_[NP];
+        const double* sp_[NS];
+        int x0, nb;
+        stream_decode<NP, NS>(vd, td, item, ob, pp_, sp_, x0, nb);
+        return sp_[NS - 1] + (int64_t)min(lane, nb - 1) * sqs;
+    };
+    if (pitem < end && lane < V) prow = prow_of(pitem);
+    if (lane < V) fence_proxy_async_global();            // acquired child writes -> async-proxy reads
+    uint32_t pseq = seq;
+    auto produce = [&]() {                               // stage chunk (pitem, pch) as sequence pseq
+        const int st = pseq % kStreamStages;
+        double* dst = buf + st * kStreamStage;
+        if (lane == 0) {
+            fence_proxy_async_smem();                    // generic reads of this stage precede the refill
+            mbar_expect_tx(bar + st, (uint32_t)(V * kStreamRow * 8));
+        }
+        __syncwarp();
+        if (lane < V) {
+            const double* a = prow + 32 * pch;
+            a -= ((uintptr_t)a >> 3) & 1;                // 16-B aligned source, data at +0 or +1
+            bulk_g2s(dst + lane * kStreamRow, a, kStreamRow * 8, bar + st);
+        }
+        ++pseq;
+        if (++pch == nch) {
+            pch = 0;
+            pitem += stride;
+            if (pitem < end && lane < V) prow = prow_of(pitem);
+        }
+    };
+    for (int k = 0; k < kStreamStages - 1 && pitem < end; ++k) produce();
+    for (int64_t item = first; item < end; item += stride) {
+        int64_t obase;
+        const double* pp[NP];
+        const double* sp[NS];
+        int x0, nb;
+        stream_decode<NP, NS>(vd, td, item, obase, pp, sp, x0, nb);
+        const int jmax = nb - 1;
+        int sh[V];                                       // staged row j starts at +0 or +1
+#pragma unroll
+        for (int j = 0; j < V; ++j) sh[j] = (int)(((uintptr_t)(sp[NS - 1] + (int64_t)min(j, jmax) * sqs) >> 3) & 1);
+        double best[V];
+        int bestC[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) { best[j] = __longlong_as_double(0x7ff0000000000000ll); bestC[j] = 0x7fffffff; }
+        for (int ch = 0; ch < nch; ++ch) {
+            if (pitem < end) produce();                  // keep kStreamStages - 1 chunks in flight
+            const int st = seq % kStreamStages;
+            mbar_wait(bar + st, (seq / kStreamStages) & 1);
+            const double* sm = buf + st * kStreamStage;
+            const int C = 32 * ch + lane;
+            if (C < K) {
+                double pre = ld(pp[0] + C);
+#pragma unroll
+                for (int t = 1; t < NP; ++t) pre = __dadd_rn(pre, ld(pp[t] + C));
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    const int jj = j < jmax ? j : jmax;
+                    double cost = pre;
+#pragma unroll
+                    for (int t = 0; t < NS - 1; ++t) cost = __dadd_rn(cost, ld(sp[t] + (int64_t)jj * sq[t] + C));
+                    cost = __dadd_rn(cost, sm[jj * kStreamRow + sh[jj] + lane]);
+                    if (cost < best[j]) { best[j] = cost; bestC[j] = C; }
+                }
+            }
+            __syncwarp();                                // every lane is done with this stage
+            ++seq;
+        }
+        // butterfly reduce-scatter across the warp (as tile_items with G = 32)
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2) {
+            const int o = 32 >> (s2 + 1);
+            const int half = V >> (s2 + 1);
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int k = 0; k < half; ++k) {
+                const double sb = up ? best[k] : best[k + half];
+                const int sc = up ? bestC[k] : bestC[k + half];
+                double kb = up ? best[k + half] : best[k];
+                int kc = up ? bestC[k + half] : bestC[k];
+                const double rb = __shfl_xor_sync(0xffffffffu, sb, o);
+                const int rc = __shfl_xor_sync(0xffffffffu, sc, o);
+                combine(kb, kc, rb, rc);
+                best[k] = kb;
+                bestC[k] = kc;
+            }
+        }
+#pragma unroll
+        for (int o = 32 >> (S + 1); o >= 1; o >>= 1) {
+            const double rb = __shfl_xor_sync(0xffffffffu, best[0], o);
+            const int rc = __shfl_xor_sync(0xffffffffu, bestC[0], o);
+            combine(best[0], bestC[0], rb, rc);
+        }
+        int jbase = 0;
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2)
+            if (lane & (32 >> (s2 + 1))) jbase += V >> (s2 + 1);
+        if ((lane & 3) == 0 && jbase < nb) st_out(vd, obase + (int64_t)(x0 + jbase) * vd.ostride_q, best[0], bestC[0]);
+        (void)H;
+    }
+    return seq;
+}
+
 // shape index: 0..63 = tiled (NP-1)*16 + NS*4 + (log2 G - 2); -1 = generic
 //   first_warp / nwarps: the calling warp's index / the warps sharing [i0, i1) (a CTA's warps
 //   are consecutive).  Item slots per warp: 32/G (throughput mode) or 1/W (latency mode).
 __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const TermDesc* td_sh,
                                           const TermDesc* tds_g, int64_t first_warp, int64_t nwarps,
-                                          int64_t i0, int64_t i1, double* red_b, int* red_c) {
+                                          int64_t i0, int64_t i1, double* red_b, int* red_c,
+                                          unsigned char* dyn, uint32_t& seq) {
     switch (shape) {
 #define PASE_CASE(NP, NS, LGG)                                                                    \
     case (NP - 1) * 16 + NS * 4 + (LGG - 2): {                                                    \
@@ -827,6 +1036,15 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
         PASE_NP1(1) PASE_NP1(2) PASE_NP1(3) PASE_NP1(4)
 #undef PASE_NP1
 #undef PASE_CASE1
+        // streaming regime: the spanning term staged by TMA bulk copies (one item per warp)
+#define PASE_CASES(NP, NS)                                                                        \
+    case kShapeStream + (NP - 1) * 4 + NS:                                                        \
+        seq = tile_stream_items<NP, NS>(vd, td_sh, i0 + first_warp, nwarps, i1, dyn, seq);        \
+        return;
+#define PASE_NPS(NP) PASE_CASES(NP, 1) PASE_CASES(NP, 2) PASE_CASES(NP, 3)
+        PASE_NPS(1) PASE_NPS(2) PASE_NPS(3) PASE_NPS(4)
+#undef PASE_NPS
+#undef PASE_CASES
 #define PASE_CASE2(NS, LGG)                                                                       \
     case kShape2D + (NS - 1) * 4 + (LGG - 2): {                                                   \
         constexpr int G_ = 1 << LGG, GPW_ = 32 / G_;                                              \
@@ -865,13 +1083,16 @@ dp_fill_vertex(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ 
     __shared__ TermDesc td[kMaxTermsSh];
     __shared__ double red_b[8 * kTile];
     __shared__ int red_c[8 * kTile];
+    extern __shared__ __align__(128) unsigned char dyn[];   // stream-tile rings (stream shapes only)
     if (threadIdx.x == 0) vd = vds[vtx];
     const int nt = min(vds[vtx].nterms, kMaxTermsSh);
     for (int t = threadIdx.x; t < nt; t += blockDim.x) td[t] = tds[vds[vtx].term0 + t];
     __syncthreads();
+    if (vd.shape >= kShapeStream) stream_init(dyn);
+    uint32_t seq = 0;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    run_shape(vd.shape, vd, td, tds, warp, nwarps, 0, vd.shape >= 0 ? vd.nitems : vd.nout, red_b, red_c);
+    run_shape(vd.shape, vd, td, tds, warp, nwarps, 0, vd.shape >= 0 ? vd.nitems : vd.nout, red_b, red_c, dyn, seq);
 }
 
 void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vertex,
@@ -881,7 +1102,13 @@ void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vert
     const int64_t units = vh.shape >= 0 ? vh.nitems : vh.nout;
     int64_t blocks = ((units * G << vh.wlog) + threads - 1) / threads;
     blocks = blocks > 148 * 8 ? 148 * 8 : (blocks < 1 ? 1 : blocks);
-    dp_fill_vertex<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(vd_dev, td_dev, vertex);
+    const size_t dyn = vh.shape >= kShapeStream ? kStreamSmemBytes : 0;
+    if (dyn) {
+        static bool attr = (cudaFuncSetAttribute(dp_fill_vertex, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)kStreamSmemBytes), true);
+        (void)attr;
+    }
+    dp_fill_vertex<<<(unsigned)blocks, threads, dyn, (cudaStream_t)stream>>>(vd_dev, td_dev, vertex);
 }
 
 // ---- persistent schedule (default): one launch runs the whole elimination tree ----------
@@ -948,7 +1175,7 @@ __global__ void __launch_bounds__(256, 2)
 dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ tds,
               const TaskDesc* __restrict__ tasks, const int32_t* __restrict__ order, int ntasks,
               int32_t* __restrict__ sched, int32_t* __restrict__ err, Peers peers, CostArgs cost,
-              int64_t* __restrict__ trace, uint64_t timeout_ns) {
+              int64_t* __restrict__ trace, uint64_t timeout_ns, int stream_smem) {
     // sched: [0] claim counter (own 128-B line), [kSchedLine, +n) pending per vertex
     int32_t* head = sched;
     int32_t* pending = sched + kSchedLine;
@@ -959,6 +1186,10 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
     __shared__ int red_c[8 * kTile];
     __shared__ int s_task;
     __shared__ CostSmem csm;                                // cost-table tasks
+    extern __shared__ __align__(128) unsigned char dyn[];   // stream-tile rings (launched with them
+    const bool stream = stream_smem != 0;                   // only when a vertex uses a stream shape)
+    if (stream) stream_init(dyn);
+    uint32_t seq = 0;                                       // this warp's staged-chunk sequence
     const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     int cur = -1;
     // a group barrier that timed out (or any earlier failure of this solve) skips the DP: the
@@ -1017,6 +1248,9 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
             if (multi) (void)ld_acquire_sys(pv);
             else if (PASE_ACQ_FENCE) fence_acquire_gpu();      // relaxed read + fence = acquire pattern
             else (void)ld_acquire(pv);
+            // the stream tile reads child tables through the async proxy (TMA): order the
+            // acquired generic-proxy writes before those reads
+            if (vd.shape >= kShapeStream) fence_proxy_async_global();
             if (trace) t_start = (int64_t)globaltimer();
         }
         __syncthreads();
@@ -1025,7 +1259,7 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
         // wave-tail tasks (schedule.cpp) run the vertex's tile with wider lane groups: every
         // tile family encodes log2(G) - 2 in the shape's low 2 bits
         const int shape = tk.glog ? ((vd.shape & ~3) | (tk.glog - 2)) : vd.shape;
-        run_shape(shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1, red_b, red_c);
+        run_shape(shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1, red_b, red_c, dyn, seq);
         int64_t t_comp = 0, t_sync = 0;
         if (trace && threadIdx.x == 0) t_comp = (int64_t)globaltimer();
         __syncthreads();                                    // task's stores precede the release
@@ -1058,10 +1292,11 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
 void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, const TaskDesc* tasks_dev,
                           const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
                           const Peers& peers, const CostArgs& cost, int nblocks, int64_t* trace_dev,
-                          uint64_t timeout_ns, void* stream) {
-    dp_persistent<<<(unsigned)nblocks, 256, 0, (cudaStream_t)stream>>>(vd_dev, td_dev, tasks_dev, order_dev,
-                                                                         ntasks, sched_dev, err_dev, peers,
-                                                                         cost, trace_dev, timeout_ns);
+                          uint64_t timeout_ns, bool stream_tiles, void* stream) {
+    const size_t dyn = stream_tiles ? kStreamSmemBytes : 0;
+    dp_persistent<<<(unsigned)nblocks, 256, dyn, (cudaStream_t)stream>>>(vd_dev, td_dev, tasks_dev, order_dev,
+                                                                           ntasks, sched_dev, err_dev, peers,
+                                                                           cost, trace_dev, timeout_ns, (int)dyn);
 }
 
 // Group barrier between the ranks of a multi-GPU search (before and after the DP): every
@@ -1084,8 +1319,13 @@ void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev,
 }
 
 int persistent_blocks_per_sm() {
+    // sized with the stream-tile rings reserved, so a context with stream shapes and one without
+    // get the same grid (2 CTAs per SM: registers bound it either way)
+    static bool attr = (cudaFuncSetAttribute(dp_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kStreamSmemBytes), true);
+    (void)attr;
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_persistent, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dp_persistent, 256, kStreamSmemBytes);
     return nb;
 }
 

@@ -172,6 +172,7 @@ constexpr int kTile1 = 4, kTile2 = 4;   // 2-D tile: outputs along qstar x q2
 constexpr int kShape2D = 64;            // shapes >= kShape2D: 2-D tiled (NS-1)*4 + (glog-2)
 constexpr int kShape2S = 96;            // shapes >= kShape2S: 2-D single-suffix ((NP0-1)*4 + form)*4 + (glog-2)
 constexpr int kShapeG1 = 160;           // shapes >= kShapeG1: 1-D tile, one lane per item (K <= 3): (NP-1)*4 + NS
+constexpr int kShapeStream = 192;       // shapes >= kShapeStream: 1-D tile, G = 32, last term TMA-staged: (NP-1)*4 + NS
 //   form 0: P1 = [A], S = [S1]; 1: P1 = [A, B], S = [S1]; 2: S = [S1, const]; 3: S = [S1, S2 on q1]
 constexpr int kMaxP0 = 4, kMaxP1 = 2;   // 2-D tile: max scalar-prefix / q2-prefix terms
 constexpr int kCostRows = 64;  // edge-table rows per cost-table CTA
@@ -229,7 +230,7 @@ void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vert
 void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, const TaskDesc* tasks_dev,
                           const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
                           const Peers& peers, const CostArgs& cost, int nblocks, int64_t* trace_dev,
-                          uint64_t timeout_ns, void* stream);
+                          uint64_t timeout_ns, bool stream_tiles, void* stream);
 void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev, uint64_t timeout_ns, void* stream);
 int persistent_blocks_per_sm();
 void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,

@@ -18,7 +18,8 @@ VARIANTS = {
     "narrow_groups": {"PASE_C_PER_LANE": "8"},
     "no_tail_no_widen": {"PASE_WAVE_TAIL": "0", "PASE_WIDEN": "0"},
     "cost_tasks": {"PASE_COST_TASKS": "1"},
-    "streaming_everywhere": {"PASE_STREAM_MB": "0"},     # every spanning child -> full-warp groups
+    "streaming_everywhere": {"PASE_STREAM_MB": "0"},     # every spanning child -> TMA-staged stream tile
+    "streaming_no_tma": {"PASE_STREAM_MB": "0", "PASE_STREAM_TMA": "0"},   # ... or full-warp 1-D tile
 }
 
 
