@@ -120,6 +120,13 @@ def fp64_peaks(sm_mhz):
                 f"derived (fallback): {SM_COUNT} SM x {FP64_LANES_PER_SM} fp64 lanes x {sm_mhz:.0f} MHz")
 
 
+def bench_config(desc, p, policy, cand, world, flush_mb=256):
+    """The `config` dict both arms print (same keys and values for the same workload and N)."""
+    return {"workload": desc, "p": p, "policy": policy, "candidates": int(cand),
+            "l2": f"GPU arm: L2 flushed ({flush_mb} MiB write) before every timed step; CPU arm: n/a",
+            "parallelism": f"dp-table partition over {world} GPU(s)"}
+
+
 def oracle_solve(graph, p, policy, threads):
     from oracle import oracle as O
     t0 = time.perf_counter()
@@ -155,12 +162,116 @@ def run_reference(args, rank, world):
         "value": value, "unit": "entries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "p": p, "policy": policy, "candidates": cand},
+        "config": bench_config(desc, p, policy, cand, world, args.flush_mb),
         "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "oracle",
                          "sample": "full workload, one complete search per step (cost tables + Fig. 5 DP)"},
         "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+    return 0
+
+
+# Table 1 of the paper: "Ours" search times in seconds, Python on a Xeon E5
+# (SandyBridge), the paper's own (unpublished) layer dims -- context only
+PAPER_TABLE1 = {
+    "alexnet": {4: 0.226, 8: 0.253, 16: 0.295, 32: 0.361, 64: 0.475},
+    "inception_v3": {4: 14.398, 8: 20.018, 16: 39.791, 32: 86.039, 64: 196.253},
+    "rnnlm": {4: 0.057, 8: 0.086, 16: 0.069, 32: 0.131, 64: 0.215},   # paper: one 5-D LSTM vertex, not unrolled
+    "transformer": {4: 9.752, 8: 28.798, 16: 130.882, 32: 553.022, 64: 1883.187},
+}
+SWEEP = [("mlp", "exact_p"), ("alexnet", "exact_p"), ("inception_v3", "exact_p"), ("rnnlm", "exact_p"),
+         ("gnmt", "exact_p"), ("gnmt4", "exact_p"), ("transformer", "exact_p"), ("transformer", "le_p")]
+
+
+def run_sweep(args):
+    """every config x p in {4, 8, 16, 32, 64} on one GPU -- device DP entries/s,
+    e2e search wall (create + solve + destroy from host arrays), algorithmic HBM and measured-ALU
+    fractions, the oracle at N threads (full search, parity checked) and at 1 thread (full search
+    when <= 1e9 candidates, else not run), and the paper's Table 1 time."""
+    import torch
+    from paper_2407_04001_b200 import pase, zoo
+    from oracle import oracle as O
+    torch.cuda.set_device(0)
+    stream = torch.cuda.Stream()
+    flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device="cuda")
+    peaks = load_peaks()
+    fp64_peak, cand_peak, _ = fp64_peaks(peaks.get("sm_max_mhz", 1965.0))
+    hbm_peak = peaks.get("hbm_gbs", 6538.0)
+    threads = os.cpu_count() or 1
+    rows = []
+    only = set(args.sweep_only.split(",")) if args.sweep_only else None
+    for key, policy in SWEEP:
+        if only and key not in only:
+            continue
+        for p in (4, 8, 16, 32, 64):
+            g = zoo.BENCH_GRAPHS[key][0]()
+            ctx = pase.Context(g, p, policy=policy, device=0, stream=stream.cuda_stream)
+            for _ in range(3):
+                r = ctx.solve()
+            ms, dp = [], []
+            for _ in range(5):
+                with torch.cuda.stream(stream):
+                    flush.fill_(1)
+                r = ctx.solve()
+                st = ctx.stats()
+                ms.append(st["ms_solve"])
+                dp.append(st["ms_dp"])
+            ctx.close()
+            cand = int(st["candidates"])
+            G = pase.Graph(g)
+            e2e = []
+            for i in range(4):
+                with torch.cuda.stream(stream):
+                    flush.fill_(1)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                with pase.Context(G, p, policy=policy, device=0, stream=stream.cuda_stream) as c2:
+                    c2.solve()
+                e1.record(stream)
+                e1.synchronize()
+                if i:
+                    e2e.append(e0.elapsed_time(e1))
+            dpm = statistics.mean(dp)
+            pol = O.EXACT_P if policy == "exact_p" else O.LE_P
+            orN = or1 = None
+            parity = None
+            if cand <= 2e10:
+                t0 = time.perf_counter()
+                Pr = O.Problem.from_model(g, p, pol)
+                o = Pr.dp(threads=threads)
+                orN = time.perf_counter() - t0
+                parity = bool(list(o["strategy"]) == list(r["config_index"]) and o["cost"] == r["cost"])
+                if cand <= 1e9:
+                    t0 = time.perf_counter()
+                    Pr = O.Problem.from_model(g, p, pol)
+                    Pr.dp(threads=1)
+                    or1 = time.perf_counter() - t0
+            row = {"config": key, "policy": policy, "p": p, "V": st["n_vertices"], "M": st["max_dep"],
+                   "K": st["max_configs"], "candidates": cand, "table_entries": int(st["table_entries"]),
+                   "solve_ms": statistics.mean(ms), "dp_ms": dpm, "e2e_ms": statistics.mean(e2e),
+                   "dp_entries_per_s": cand / (dpm / 1e3),
+                   "alg_hbm_gbs": st["alg_bytes_dp"] / (dpm / 1e3) / 1e9,
+                   "alg_hbm_frac": st["alg_bytes_dp"] / (dpm / 1e3) / 1e9 / hbm_peak,
+                   "alu_frac": st["dp_fp64_ops"] / (dpm / 1e3) / 1e12 / fp64_peak,
+                   "cand_frac": (cand / (dpm / 1e3) / cand_peak) if cand_peak else None,
+                   "oracle_1thr_s": or1, "oracle_nthr_s": orN, "oracle_threads": threads, "parity": parity,
+                   "paper_s": PAPER_TABLE1.get(key, {}).get(p) if policy == "exact_p" else None}
+            rows.append(row)
+            print(json.dumps(row), flush=True)
+    def f(x, fmt):
+        return "–" if x is None else format(x, fmt)
+    lines = ["| Config | p / policy | |V| | M | K max | Σ candidates | solve ms (DP ms) | e2e search ms | DP entries/s | alg. HBM GB/s (% of 6539) | ALU % (DADD) | cand. % | oracle 1-thr s | oracle N-thr s | parity | paper s |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+    for r in rows:
+        lines.append(f"| {r['config']} | {r['p']} / {r['policy'].upper()} | {r['V']} | {r['M']} | {r['K']} | {r['candidates']:.3g} | "
+                     f"{r['solve_ms']:.3f} ({r['dp_ms']:.3f}) | {r['e2e_ms']:.3f} | {r['dp_entries_per_s']:.3g} | "
+                     f"{r['alg_hbm_gbs']:.0f} ({100 * r['alg_hbm_frac']:.1f} %) | {100 * r['alu_frac']:.1f} | "
+                     f"{f(None if r['cand_frac'] is None else 100 * r['cand_frac'], '.1f')} | {f(r['oracle_1thr_s'], '.3f')} | "
+                     f"{f(r['oracle_nthr_s'], '.3f')} (N={r['oracle_threads']}) | {r['parity']} | {f(r['paper_s'], '.3f')} |")
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    open(os.path.join(ROOT, "gpurun_out", "sweep.md"), "w").write("\n".join(lines) + "\n")
+    json.dump(rows, open(os.path.join(ROOT, "gpurun_out", "sweep.json"), "w"), indent=1)
     return 0
 
 
@@ -175,7 +286,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--flush-mb", type=int, default=256)
     ap.add_argument("--no-alt", action="store_true", help="skip the throughput-regime (LE_P) line")
+    ap.add_argument("--sweep", action="store_true", help="BASELINE.md §4 table: every config x p on one GPU")
+    ap.add_argument("--sweep-only", default="", help="comma-separated config keys for --sweep")
     args = ap.parse_args()
+    if args.sweep:
+        return run_sweep(args)
     args.warmup = max(args.warmup, 3)
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
     local_rank = env_int("LOCAL_RANK", 0)
@@ -287,7 +402,10 @@ def main():
         c3.close()
         alt = {"workload": adesc, "value": int(ast["candidates"]) * len(a_ms) / (a_tot / 1e3), "unit": "entries/s",
                "steps": len(a_ms), "ms_per_step": a_tot / len(a_ms), "dp_fill_ms": statistics.mean(a_dp),
-               "candidates": int(ast["candidates"]), "dp_fp64_ops": int(ast["dp_fp64_ops"])}
+               "candidates": int(ast["candidates"]), "dp_fp64_ops": int(ast["dp_fp64_ops"]),
+               "alg_bytes_dp": int(ast["alg_bytes_dp"]),
+               "partitioned": f"{world} rank(s); multi-GPU partitions {int(ast['comm_bytes'])} B of peer stores per rank per solve",
+               "comm_bytes_per_rank": int(ast["comm_bytes"])}
 
     # e2e through the public API with host inputs (create + solve + destroy per step): the
     # graph is held in the C ABI's input layout (pase.Graph: pase_graph node / edge arrays in
@@ -360,11 +478,10 @@ def main():
         "value": value, "unit": "entries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "p": p, "policy": policy, "vertices": st["n_vertices"],
-                   "candidates": cand, "table_entries": int(st["table_entries"]), "M": st["max_dep"],
-                   "K": st["max_configs"], "tree_levels": st["tree_levels"],
-                   "l2": f"flushed ({args.flush_mb} MiB write) before every timed step",
-                   "parallelism": f"dp-table partition over {world} GPU(s)"},
+        "config": bench_config(desc, p, policy, cand, world, args.flush_mb),
+        "plan": {"vertices": st["n_vertices"], "table_entries": int(st["table_entries"]), "M": st["max_dep"],
+                 "K": st["max_configs"], "tree_levels": st["tree_levels"],
+                 "comm_bytes_per_rank": int(st["comm_bytes"])},
         "phases_ms": {"tables": statistics.mean(tab_ms), "dp_fill": mean_dp,
                       "solve_total": statistics.mean(step_ms)},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
