@@ -1019,11 +1019,15 @@ pase_status pase_create(const pase_graph* g, int32_t p, const pase_machine* m, p
     if (st) return fail(st);
     auto t_upload = std::chrono::steady_clock::now();
     if ((st = record_graph(ctx))) return fail(st);
-    // the pools are complete before any other stream (a peer's, the legacy one used by the
-    // introspection hooks) touches them
-    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) { ctx->err = "cudaStreamSynchronize failed"; return fail(PASE_ERR_CUDA); }
-    stage_put(ctx->stage_block);
-    ctx->stage_block = nullptr;
+    // A group's pools are read by the peers' kernels (their own streams): complete them before
+    // returning.  A single-GPU context touches its pools only through its own stream (solves and
+    // every hook are ordered there), so the upload stays asynchronous and the pinned image goes
+    // back to the cache once the first solve (or destroy) has synchronised the stream.
+    if (ctx->world > 1) {
+        if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) { ctx->err = "cudaStreamSynchronize failed"; return fail(PASE_ERR_CUDA); }
+        stage_put(ctx->stage_block);
+        ctx->stage_block = nullptr;
+    }
     auto t_graph = std::chrono::steady_clock::now();
     fill_stats(ctx);
     using ms = std::chrono::duration<double, std::milli>;
@@ -1071,6 +1075,10 @@ pase_status pase_finish(pase_ctx* ctx, int32_t* configs_out, int32_t* config_ind
     NvtxRange r("pase_finish (wait + strategy)");
     CUDA_TRY(cudaSetDevice(ctx->dev));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (ctx->stage_block) {                     // the create-time upload has completed
+        stage_put(ctx->stage_block);
+        ctx->stage_block = nullptr;
+    }
     if (*ctx->h_err) {
         const int code = *ctx->h_err;
         ctx->err = code == 3 ? std::string("DP entry without a finite candidate (cost overflow): no strategy")
