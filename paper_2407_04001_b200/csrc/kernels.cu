@@ -1387,7 +1387,7 @@ backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt
         if (hc) hc[v] = c;
     }
     if (threadIdx.x == 0) {
-        const double t = root_T[0];                         // f(|V|, ∅)
+        const double t = failed ? 0.0 : root_T[0];          // f(|V|, ∅); unwritten after a failure
         *total = t;
         if (host_out) {
             *reinterpret_cast<double*>(host_out) = t;
