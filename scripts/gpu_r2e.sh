@@ -11,4 +11,5 @@ python scripts/ncu_summary.py /tmp/prof_stream_tma.ncu-rep > gpurun_out/ncu_stre
 ncu -i /tmp/prof_stream_tma.ncu-rep --page raw --csv > gpurun_out/ncu_stream_tma_raw.csv 2>/dev/null
 timeout 2400 python -m pytest tests -m gpu -x -q 2>&1 | tail -6
 timeout 1800 python bench.py --sweep > gpurun_out/sweep.log 2>&1; tail -2 gpurun_out/sweep.log
+PASE_TIMING=1 timeout 300 python scripts/e2e_probe.py transformer > gpurun_out/e2e_probe.log 2>&1
 timeout 600 python bench.py --steps 50 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
