@@ -71,7 +71,11 @@ struct pase_ctx {
     // pool 2: scheduler (pending counters written by peers), tasks, claim order, trace
     void* pool2 = nullptr;
     size_t pool2_bytes = 0;
-    int32_t* d_sched = nullptr;             // [0] claim counter | [kSchedLine, +n) pending
+    int32_t* d_sched = nullptr;             // [0] claim counter / ring head | [kSchedLine, +n) pending |
+                                            // ready queue: tail line, ring[ntasks]
+    int32_t* d_ring = nullptr;              // ready-queue mode (nullptr: static claim order)
+    int32_t* d_ring_tail = nullptr;
+    bool queue = false;
     int32_t* d_sched_init = nullptr;        // its solve-start image
     size_t sched_bytes = 0;
     int32_t* d_bar = nullptr;               // [0] arrivals, [kSchedLine] epoch
@@ -641,15 +645,22 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     // tasks, broadcast flags, pending counters, claim order (schedule.cpp)
     std::vector<int32_t> consumer(chunks.size());
     for (size_t k = 0; k < chunks.size(); ++k) consumer[k] = chunks[k].consumer;
+    // ready queue (single GPU; PASE_QUEUE=0 selects the static order)
+    const char* qv = std::getenv("PASE_QUEUE");
+    ctx->queue = ctx->world == 1 && !ctx->cost_tasks && !(qv && qv[0] == '0');
     pase_status st = pase::build_schedule(P, ctx->vd, ctx->world, ctx->rank, ctx->nblocks, ctx->sp, ctx->err,
-                                          ctx->cost_tasks ? &consumer : nullptr);
+                                          ctx->cost_tasks ? &consumer : nullptr, !ctx->queue);
     if (st) return st;
     ctx->ntasks = (int)ctx->sp.tasks.size();
     ctx->total_tasks = ctx->sp.total_tasks;
     for (VertexDesc& d : ctx->vd) d.npeer = d.bcast ? ctx->world - 1 : 0;
     const auto p3 = clk::now();
     // pool 2
-    const size_t sched_words = pase::kSchedLine + (size_t)n;
+    // ready queue: tail on its own line after the pending counters, then one ring slot per
+    // task; reset with the rest of the block
+    const size_t pend_words = ((size_t)n + pase::kSchedLine - 1) / pase::kSchedLine * pase::kSchedLine;
+    const size_t ring_off = pase::kSchedLine + pend_words + pase::kSchedLine;
+    const size_t sched_words = ctx->queue ? ring_off + std::max<size_t>(ctx->sp.tasks.size(), 1) : pase::kSchedLine + (size_t)n;
     ctx->sched_bytes = sizeof(int32_t) * sched_words;
     std::vector<Item> items2 = {                          // uploaded items first, as pool 1
         {(void**)&ctx->d_sched_init, ctx->sched_bytes},
@@ -662,6 +673,15 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     if ((st = carve(ctx, items2, &ctx->pool2, &ctx->pool2_bytes, device))) return st;
     std::vector<int32_t> sched(sched_words, 0);
     for (int i = 0; i < n; ++i) sched[pase::kSchedLine + i] = ctx->sp.pending[i];
+    ctx->d_ring = ctx->d_ring_tail = nullptr;
+    if (ctx->queue) {                           // the leaves' tasks are published from the start
+        for (size_t k = 0; k < ctx->sp.ready0.size(); ++k) sched[ring_off + k] = ctx->sp.ready0[k] + 1;
+        sched[ring_off - pase::kSchedLine] = (int32_t)ctx->sp.ready0.size();
+        if (ctx->d_sched) {
+            ctx->d_ring = ctx->d_sched + ring_off;
+            ctx->d_ring_tail = ctx->d_sched + ring_off - pase::kSchedLine;
+        }
+    }
     // single-rank peer table (connect() fills the group's)
     ctx->peers = pase::Peers{};
     ctx->peers.world = ctx->world;
@@ -782,7 +802,8 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
         if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, ctx->timeout_ns, s);
         pase::launch_dp_persistent(ctx->d_vd, ctx->d_td, ctx->d_tasks, ctx->d_order, ctx->ntasks, ctx->d_sched,
                                    d_err, ctx->peers, cost_args(ctx), ctx->nblocks,
-                                   trace_on() ? ctx->d_trace : nullptr, ctx->timeout_ns, ctx->stream_tiles, s);
+                                   trace_on() ? ctx->d_trace : nullptr, ctx->timeout_ns, ctx->stream_tiles,
+                                   ctx->d_ring, ctx->d_ring_tail, s);
         if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, ctx->timeout_ns, s);
     } else {
         CUDA_TRY(cudaEventRecord(start, s));

@@ -1171,14 +1171,28 @@ __device__ __forceinline__ bool timed_out(uint64_t t0, uint64_t limit_ns) {
     return limit_ns != 0 && globaltimer() - t0 > limit_ns;
 }
 
+__device__ __forceinline__ void st_release(int32_t* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Claim modes.  STATIC (multi-GPU groups; PASE_QUEUE=0): CTAs take tasks in the host's static
+// topological order and wait on each claimed task's pending counter.  READY QUEUE (single GPU,
+// default): only tasks whose dependencies are met are ever claimed -- the CTA that releases a
+// vertex's last child task (its pending counter 1 -> 0) publishes all of the vertex's tasks into
+// a ring (st.release of id + 1 per slot); CTAs claim ring slots with a fetch-and-add and wait
+// only while the ring is empty.  No CTA ever sits on a claimed task whose children are still
+// running, so ready work -- the critical path above all -- never queues behind blocked CTAs.
 __global__ void __launch_bounds__(256, 2)
 dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ tds,
               const TaskDesc* __restrict__ tasks, const int32_t* __restrict__ order, int ntasks,
               int32_t* __restrict__ sched, int32_t* __restrict__ err, Peers peers, CostArgs cost,
-              int64_t* __restrict__ trace, uint64_t timeout_ns, int stream_smem) {
-    // sched: [0] claim counter (own 128-B line), [kSchedLine, +n) pending per vertex
+              int64_t* __restrict__ trace, uint64_t timeout_ns, int stream_smem, int32_t* __restrict__ ring,
+              int32_t* __restrict__ ring_tail) {
+    // sched: [0] claim counter / ring head (own 128-B line), [kSchedLine, +n) pending per vertex
     int32_t* head = sched;
     int32_t* pending = sched + kSchedLine;
+    const bool queue = ring != nullptr;
+    __shared__ int s_push;
     const bool multi = peers.world > 1;                     // peers: .sys scope
     __shared__ VertexDesc vd;
     __shared__ TermDesc td[kMaxTermsSh];
@@ -1200,7 +1214,21 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
         if (threadIdx.x == 0) {
             if (trace) t_claim = (int64_t)globaltimer();
             const int s = atomicAdd(head, 1);
-            s_task = s < ntasks ? order[s] : -1;
+            if (!queue) {
+                s_task = s < ntasks ? order[s] : -1;
+            } else if (s >= ntasks) {
+                s_task = -1;
+            } else {                                        // wait until slot s is published
+                int v = ld_relaxed(ring + s);
+                if (v == 0) {
+                    const uint64_t t0 = globaltimer();
+                    while ((v = ld_relaxed(ring + s)) == 0)
+                        if (timed_out(t0, timeout_ns)) { atomicExch(err, 1); break; }
+                }
+                fence_acquire_gpu();                        // acquire: the children's tables
+                s_task = v - 1;
+                if (trace) t_start = (int64_t)globaltimer();
+            }
         }
         __syncthreads();
         int task = s_task;
@@ -1232,7 +1260,9 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
             for (int k = threadIdx.x; k < nt; k += blockDim.x) td[k] = tds[vd.term0 + k];
             cur = tk.vtx;
         }
-        if (threadIdx.x == 0) {                             // wait for the children's tasks
+        if (queue) {
+            // ready by construction; TMA reads of the children need the proxy fence (tile entry)
+        } else if (threadIdx.x == 0) {                      // wait for the children's tasks
             int32_t* pv = pending + tk.vtx;
             if ((multi ? ld_relaxed_sys(pv) : ld_relaxed(pv)) != 0) {
                 unsigned bo = 32;
@@ -1263,6 +1293,32 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
         int64_t t_comp = 0, t_sync = 0;
         if (trace && threadIdx.x == 0) t_comp = (int64_t)globaltimer();
         __syncthreads();                                    // task's stores precede the release
+        if (queue) {
+            if (threadIdx.x == 0) {
+                if (trace) t_sync = (int64_t)globaltimer();
+                s_push = -1;
+                if (vd.parent >= 0 && atom_add_acq_rel(pending + vd.parent, -1) == 1) {
+                    // last child task: the parent is ready -- reserve its slots
+                    const int nt = vds[vd.parent].ntasks;
+                    s_push = atomicAdd(ring_tail, nt);
+                }
+            }
+            __syncthreads();
+            if (s_push >= 0) {                              // publish the parent's tasks
+                const int t0 = vds[vd.parent].task0, nt = vds[vd.parent].ntasks;
+                for (int k = threadIdx.x; k < nt; k += blockDim.x) st_release(ring + s_push + k, t0 + k + 1);
+            }
+            if (threadIdx.x == 0 && trace) {
+                int64_t* tr = trace + (int64_t)kTraceWords * task;
+                tr[0] = ((int64_t)smid() << 32) | (uint32_t)tk.vtx;
+                tr[1] = t_claim;
+                tr[2] = t_start;
+                tr[3] = t_comp;
+                tr[4] = t_sync;
+                tr[5] = (int64_t)globaltimer();
+            }
+            continue;
+        }
         if (threadIdx.x == 0) {
             if (trace) t_sync = (int64_t)globaltimer();
             if (vd.parent >= 0) {
@@ -1292,11 +1348,13 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
 void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, const TaskDesc* tasks_dev,
                           const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
                           const Peers& peers, const CostArgs& cost, int nblocks, int64_t* trace_dev,
-                          uint64_t timeout_ns, bool stream_tiles, void* stream) {
+                          uint64_t timeout_ns, bool stream_tiles, int32_t* ring, int32_t* ring_tail,
+                          void* stream) {
     const size_t dyn = stream_tiles ? kStreamSmemBytes : 0;
     dp_persistent<<<(unsigned)nblocks, 256, dyn, (cudaStream_t)stream>>>(vd_dev, td_dev, tasks_dev, order_dev,
                                                                            ntasks, sched_dev, err_dev, peers,
-                                                                           cost, trace_dev, timeout_ns, (int)dyn);
+                                                                           cost, trace_dev, timeout_ns, (int)dyn,
+                                                                           ring, ring_tail);
 }
 
 // Group barrier between the ranks of a multi-GPU search (before and after the DP): every

@@ -156,6 +156,7 @@ struct SchedPlan {           // build_schedule output for one rank
     std::vector<TaskDesc> tasks;   // this rank's tasks, vertex-major (VertexDesc.task0)
     std::vector<int32_t> order;    // claim order (indices into tasks)
     std::vector<int32_t> pending;  // initial pending counter per vertex
+    std::vector<int32_t> ready0;   // ready-queue mode: tasks ready at the start (no children), in order
     int64_t total_tasks = 0;       // over all ranks
 };
 
@@ -166,7 +167,7 @@ struct SchedPlan {           // build_schedule output for one rank
 // tasks wait for.
 pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world, int rank, int nblocks,
                            SchedPlan& out, std::string& err,
-                           const std::vector<int32_t>* chunk_consumer = nullptr);
+                           const std::vector<int32_t>* chunk_consumer = nullptr, bool simulate = true);
 constexpr int kTile = 8;     // max outputs per lane group along qstar
 constexpr int kTile1 = 4, kTile2 = 4;   // 2-D tile: outputs along qstar x q2
 constexpr int kShape2D = 64;            // shapes >= kShape2D: 2-D tiled (NS-1)*4 + (glog-2)
@@ -230,7 +231,8 @@ void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vert
 void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, const TaskDesc* tasks_dev,
                           const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
                           const Peers& peers, const CostArgs& cost, int nblocks, int64_t* trace_dev,
-                          uint64_t timeout_ns, bool stream_tiles, void* stream);
+                          uint64_t timeout_ns, bool stream_tiles, int32_t* ring, int32_t* ring_tail,
+                          void* stream);
 void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev, uint64_t timeout_ns, void* stream);
 int persistent_blocks_per_sm();
 void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,

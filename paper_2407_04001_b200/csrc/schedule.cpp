@@ -30,7 +30,8 @@ namespace pase {
 static const bool kWaveTail = !(std::getenv("PASE_WAVE_TAIL") && std::getenv("PASE_WAVE_TAIL")[0] == '0');
 
 pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world, int rank, int nblocks,
-                           SchedPlan& out, std::string& err, const std::vector<int32_t>* chunk_consumer) {
+                           SchedPlan& out, std::string& err, const std::vector<int32_t>* chunk_consumer,
+                           bool simulate) {
     const int n = P.n;
     const int G = std::max(world, 1);
     nblocks = std::max(nblocks, 1);
@@ -153,7 +154,11 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     for (int i = n; i < nv; ++i) bl[i] = 4.0 + bl[i - n];
     const auto tt1 = std::chrono::steady_clock::now();
     std::vector<double> start(ntk, -1.0);
-    {
+    if (!simulate) {
+        // ready-queue claiming (single GPU): the order only ranks the leaves' tasks published at
+        // the start -- critical path (bottom level) first; no list-schedule simulation
+        for (int64_t t = 0; t < ntk; ++t) start[t] = -bl[all[t].vtx];
+    } else {
         // ready (vertex, rank) runs: all tasks of a vertex share its priority, so the heap holds
         // one entry per released run and a cursor walks the run's tasks
         using RT = std::pair<double, int32_t>;                         // (priority, -(v*G+q))
@@ -235,6 +240,9 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
             out.tasks.push_back({(int32_t)(-1 - all[t].i0), 0, 0, 0});
         }
     for (int32_t t : mine) out.order.push_back(local_id[t]);
+    out.ready0.clear();                                 // leaves, in the static order's priority
+    for (int32_t t : out.order)
+        if (out.tasks[t].vtx >= 0 && out.pending[out.tasks[t].vtx] == 0) out.ready0.push_back(t);
     out.total_tasks = ntk;
     return PASE_OK;
 }
