@@ -645,9 +645,11 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     // tasks, broadcast flags, pending counters, claim order (schedule.cpp)
     std::vector<int32_t> consumer(chunks.size());
     for (size_t k = 0; k < chunks.size(); ++k) consumer[k] = chunks[k].consumer;
-    // ready queue (single GPU; PASE_QUEUE=0 selects the static order)
+    // ready queue (single GPU, opt-in PASE_QUEUE=1): measured SLOWER than the static critical-path
+    // order on every workload (profiles/r02_ab_queue.txt: FIFO publication loses the priority, and
+    // non-critical ready work competes with the critical chain for the SMs)
     const char* qv = std::getenv("PASE_QUEUE");
-    ctx->queue = ctx->world == 1 && !ctx->cost_tasks && !(qv && qv[0] == '0');
+    ctx->queue = ctx->world == 1 && !ctx->cost_tasks && qv && qv[0] == '1';
     pase_status st = pase::build_schedule(P, ctx->vd, ctx->world, ctx->rank, ctx->nblocks, ctx->sp, ctx->err,
                                           ctx->cost_tasks ? &consumer : nullptr, !ctx->queue);
     if (st) return st;

@@ -1175,9 +1175,10 @@ __device__ __forceinline__ void st_release(int32_t* p, int v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Claim modes.  STATIC (multi-GPU groups; PASE_QUEUE=0): CTAs take tasks in the host's static
-// topological order and wait on each claimed task's pending counter.  READY QUEUE (single GPU,
-// default): only tasks whose dependencies are met are ever claimed -- the CTA that releases a
+// Claim modes.  STATIC (default): CTAs take tasks in the host's static topological order (a
+// critical-path list schedule) and wait on each claimed task's pending counter.  READY QUEUE
+// (single GPU, opt-in PASE_QUEUE=1; measured slower, profiles/r02_ab_queue.txt): only tasks whose
+// dependencies are met are ever claimed -- the CTA that releases a
 // vertex's last child task (its pending counter 1 -> 0) publishes all of the vertex's tasks into
 // a ring (st.release of id + 1 per slot); CTAs claim ring slots with a fetch-and-add and wait
 // only while the ring is empty.  No CTA ever sits on a claimed task whose children are still

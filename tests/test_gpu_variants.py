@@ -20,7 +20,7 @@ VARIANTS = {
     "cost_tasks": {"PASE_COST_TASKS": "1"},
     "streaming_everywhere": {"PASE_STREAM_MB": "0"},     # every spanning child -> TMA-staged stream tile
     "streaming_no_tma": {"PASE_STREAM_MB": "0", "PASE_STREAM_TMA": "0"},   # ... or full-warp 1-D tile
-    "static_order": {"PASE_QUEUE": "0"},                  # static claim order instead of the ready queue
+    "ready_queue": {"PASE_QUEUE": "1"},                   # ready-queue claiming instead of the static order
 }
 
 
