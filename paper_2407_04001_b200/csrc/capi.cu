@@ -393,9 +393,11 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
     d.shape = pase::kShape2D + (NS - 1) * 4 + (d.glog - 2);
 }
 
-bool stream_tma() {
-    static const bool on = !(std::getenv("PASE_STREAM_TMA") && std::getenv("PASE_STREAM_TMA")[0] == '0');
-    return on;
+// streaming-vertex form (PASE_STREAM_TMA): 0 = direct full-warp loads, 1 = rows TMA-staged in a
+// shared-memory ring, 2 = direct loads with the next item's rows TMA-prefetched into L2
+int stream_tma() {
+    static const int mode = std::getenv("PASE_STREAM_TMA") ? std::atoi(std::getenv("PASE_STREAM_TMA")) : 2;
+    return mode;
 }
 
 // streaming-regime vertices: spanning child tables of at least this many bytes
@@ -616,7 +618,8 @@ pase_status prepare(pase_ctx* ctx, bool device) {
                 d.glog = 5;
                 d.shape = (NP - 1) * 16 + NS * 4 + 3;
                 // its rows staged into shared memory by TMA bulk copies
-                if (last_spans && NS >= 1 && stream_tma()) d.shape = pase::kShapeStream + (NP - 1) * 4 + NS;
+                if (last_spans && NS >= 1 && stream_tma() == 1) d.shape = pase::kShapeStream + (NP - 1) * 4 + NS;
+                if (last_spans && NS >= 1 && stream_tma() == 2) d.shape = pase::kShapeStreamPF + (NP - 1) * 4 + NS;
             } else if (d.wlog == 0 && d.K <= 3) {             // one lane per item
                 d.glog = 0;
                 d.shape = pase::kShapeG1 + (NP - 1) * 4 + NS;
@@ -631,7 +634,7 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     const auto p1 = clk::now();
     widen_critical(ctx);
     ctx->stream_tiles = false;
-    for (const VertexDesc& d : ctx->vd) ctx->stream_tiles = ctx->stream_tiles || d.shape >= pase::kShapeStream;
+    for (const VertexDesc& d : ctx->vd) ctx->stream_tiles = ctx->stream_tiles || pase::stream_smem_shape(d.shape);
     for (VertexDesc& d : ctx->vd) {                       // partitioned item order (split_item)
         d.psub = (d.part && d.shape >= 0) ? (int32_t)(d.ncombo / d.radix[d.m - 1]) : 1;
         // magic numbers of the work-item decode (division by invariant integers)

@@ -1002,6 +1002,98 @@ __device__ __noinline__ uint32_t tile_stream_items(const VertexDesc& vd, const T
     return seq;
 }
 
+// Streaming-regime tile, L2-prefetch form: the 1-D tile with one item per warp (G = 32) reading
+// the spanning rows with coalesced 256-B loads, while lanes 0..kTile-1 hand the NEXT item's rows
+// to the TMA unit as bulk L2 prefetches (cp.async.bulk.prefetch.L2) -- the HBM stream runs one
+// item ahead of the loads, with no shared-memory round trip and no per-chunk synchronisation.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "r"(bytes) : "memory");
+}
+
+template <int NP, int NS>
+__device__ __noinline__ void tile_stream_pf(const VertexDesc& vd, const TermDesc* td, int64_t first,
+                                            int64_t stride, int64_t end) {
+    constexpr int V = kTile, S = 3;
+    const int lane = threadIdx.x & 31;
+    const int q = vd.qstar;
+    const int K = vd.K;
+    const int64_t sqs = td[NP + NS - 1].stride[q];
+    int sq[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) sq[t] = (int)td[NP + t].stride[q];
+    // one row = K doubles from an 8-B aligned start: prefetch the 16-B aligned cover
+    auto prefetch_rows = [&](int64_t item) {
+        int64_t ob;
+        const double* pp_[NP];
+        const double* sp_[NS];
+        int x0, nb;
+        stream_decode<NP, NS>(vd, td, item, ob, pp_, sp_, x0, nb);
+        if (lane < nb) {
+            const uintptr_t a = (uintptr_t)(sp_[NS - 1] + (int64_t)lane * sqs);
+            const uintptr_t lo = a & ~(uintptr_t)15, hi = (a + (uintptr_t)K * 8 + 15) & ~(uintptr_t)15;
+            bulk_prefetch_l2((const void*)lo, (uint32_t)(hi - lo));
+        }
+    };
+    if (first < end && lane < V) prefetch_rows(first);
+    for (int64_t item = first; item < end; item += stride) {
+        if (item + stride < end && lane < V) prefetch_rows(item + stride);
+        int64_t obase;
+        const double* pp[NP];
+        const double* sp[NS];
+        int x0, nb;
+        stream_decode<NP, NS>(vd, td, item, obase, pp, sp, x0, nb);
+        const int jmax = nb - 1;
+        double best[V];
+        int bestC[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) { best[j] = __longlong_as_double(0x7ff0000000000000ll); bestC[j] = 0x7fffffff; }
+#pragma unroll 2
+        for (int C = lane; C < K; C += 32) {
+            double pre = ld(pp[0] + C);
+#pragma unroll
+            for (int t = 1; t < NP; ++t) pre = __dadd_rn(pre, ld(pp[t] + C));
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const int jj = j < jmax ? j : jmax;
+                double cost = pre;
+#pragma unroll
+                for (int t = 0; t < NS - 1; ++t) cost = __dadd_rn(cost, ld(sp[t] + (int64_t)jj * sq[t] + C));
+                cost = __dadd_rn(cost, ld(sp[NS - 1] + (int64_t)jj * sqs + C));
+                if (cost < best[j]) { best[j] = cost; bestC[j] = C; }
+            }
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2) {
+            const int o = 32 >> (s2 + 1);
+            const int half = V >> (s2 + 1);
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int k = 0; k < half; ++k) {
+                const double sb = up ? best[k] : best[k + half];
+                const int sc = up ? bestC[k] : bestC[k + half];
+                double kb = up ? best[k + half] : best[k];
+                int kc = up ? bestC[k + half] : bestC[k];
+                const double rb = __shfl_xor_sync(0xffffffffu, sb, o);
+                const int rc = __shfl_xor_sync(0xffffffffu, sc, o);
+                combine(kb, kc, rb, rc);
+                best[k] = kb;
+                bestC[k] = kc;
+            }
+        }
+#pragma unroll
+        for (int o = 32 >> (S + 1); o >= 1; o >>= 1) {
+            const double rb = __shfl_xor_sync(0xffffffffu, best[0], o);
+            const int rc = __shfl_xor_sync(0xffffffffu, bestC[0], o);
+            combine(best[0], bestC[0], rb, rc);
+        }
+        int jbase = 0;
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2)
+            if (lane & (32 >> (s2 + 1))) jbase += V >> (s2 + 1);
+        if ((lane & 3) == 0 && jbase < nb) st_out(vd, obase + (int64_t)(x0 + jbase) * vd.ostride_q, best[0], bestC[0]);
+    }
+}
+
 // shape index: 0..63 = tiled (NP-1)*16 + NS*4 + (log2 G - 2); -1 = generic
 //   first_warp / nwarps: the calling warp's index / the warps sharing [i0, i1) (a CTA's warps
 //   are consecutive).  Item slots per warp: 32/G (throughput mode) or 1/W (latency mode).
@@ -1045,6 +1137,15 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
         PASE_NPS(1) PASE_NPS(2) PASE_NPS(3) PASE_NPS(4)
 #undef PASE_NPS
 #undef PASE_CASES
+        // streaming regime: direct coalesced loads, the next item's rows bulk-prefetched into L2
+#define PASE_CASEP(NP, NS)                                                                        \
+    case kShapeStreamPF + (NP - 1) * 4 + NS:                                                      \
+        tile_stream_pf<NP, NS>(vd, td_sh, i0 + first_warp, nwarps, i1);                           \
+        return;
+#define PASE_NPP(NP) PASE_CASEP(NP, 1) PASE_CASEP(NP, 2) PASE_CASEP(NP, 3)
+        PASE_NPP(1) PASE_NPP(2) PASE_NPP(3) PASE_NPP(4)
+#undef PASE_NPP
+#undef PASE_CASEP
 #define PASE_CASE2(NS, LGG)                                                                       \
     case kShape2D + (NS - 1) * 4 + (LGG - 2): {                                                   \
         constexpr int G_ = 1 << LGG, GPW_ = 32 / G_;                                              \
@@ -1088,7 +1189,7 @@ dp_fill_vertex(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ 
     const int nt = min(vds[vtx].nterms, kMaxTermsSh);
     for (int t = threadIdx.x; t < nt; t += blockDim.x) td[t] = tds[vds[vtx].term0 + t];
     __syncthreads();
-    if (vd.shape >= kShapeStream) stream_init(dyn);
+    if (stream_smem_shape(vd.shape)) stream_init(dyn);
     uint32_t seq = 0;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1102,7 +1203,7 @@ void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vert
     const int64_t units = vh.shape >= 0 ? vh.nitems : vh.nout;
     int64_t blocks = ((units * G << vh.wlog) + threads - 1) / threads;
     blocks = blocks > 148 * 8 ? 148 * 8 : (blocks < 1 ? 1 : blocks);
-    const size_t dyn = vh.shape >= kShapeStream ? kStreamSmemBytes : 0;
+    const size_t dyn = stream_smem_shape(vh.shape) ? kStreamSmemBytes : 0;
     if (dyn) {
         static bool attr = (cudaFuncSetAttribute(dp_fill_vertex, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)kStreamSmemBytes), true);
@@ -1281,7 +1382,7 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
             else (void)ld_acquire(pv);
             // the stream tile reads child tables through the async proxy (TMA): order the
             // acquired generic-proxy writes before those reads
-            if (vd.shape >= kShapeStream) fence_proxy_async_global();
+            if (stream_smem_shape(vd.shape)) fence_proxy_async_global();
             if (trace) t_start = (int64_t)globaltimer();
         }
         __syncthreads();

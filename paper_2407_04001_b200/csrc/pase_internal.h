@@ -173,7 +173,12 @@ constexpr int kTile1 = 4, kTile2 = 4;   // 2-D tile: outputs along qstar x q2
 constexpr int kShape2D = 64;            // shapes >= kShape2D: 2-D tiled (NS-1)*4 + (glog-2)
 constexpr int kShape2S = 96;            // shapes >= kShape2S: 2-D single-suffix ((NP0-1)*4 + form)*4 + (glog-2)
 constexpr int kShapeG1 = 160;           // shapes >= kShapeG1: 1-D tile, one lane per item (K <= 3): (NP-1)*4 + NS
-constexpr int kShapeStream = 192;       // shapes >= kShapeStream: 1-D tile, G = 32, last term TMA-staged: (NP-1)*4 + NS
+constexpr int kShapeStream = 192;       // [192, 224): 1-D tile, G = 32, last term TMA-staged in smem: (NP-1)*4 + NS
+constexpr int kShapeStreamPF = 224;     // [224, 256): 1-D tile, G = 32, next item's last-term rows TMA-prefetched to L2
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr bool stream_smem_shape(int s) { return s >= kShapeStream && s < kShapeStreamPF; }
 //   form 0: P1 = [A], S = [S1]; 1: P1 = [A, B], S = [S1]; 2: S = [S1, const]; 3: S = [S1, S2 on q1]
 constexpr int kMaxP0 = 4, kMaxP1 = 2;   // 2-D tile: max scalar-prefix / q2-prefix terms
 constexpr int kCostRows = 64;  // edge-table rows per cost-table CTA

@@ -18,8 +18,9 @@ VARIANTS = {
     "narrow_groups": {"PASE_C_PER_LANE": "8"},
     "no_tail_no_widen": {"PASE_WAVE_TAIL": "0", "PASE_WIDEN": "0"},
     "cost_tasks": {"PASE_COST_TASKS": "1"},
-    "streaming_everywhere": {"PASE_STREAM_MB": "0"},     # every spanning child -> TMA-staged stream tile
-    "streaming_no_tma": {"PASE_STREAM_MB": "0", "PASE_STREAM_TMA": "0"},   # ... or full-warp 1-D tile
+    "streaming_everywhere": {"PASE_STREAM_MB": "0"},     # every spanning child -> stream tile (L2 prefetch)
+    "streaming_smem_ring": {"PASE_STREAM_MB": "0", "PASE_STREAM_TMA": "1"},  # ... TMA smem ring
+    "streaming_no_tma": {"PASE_STREAM_MB": "0", "PASE_STREAM_TMA": "0"},   # ... or plain full-warp 1-D tile
     "ready_queue": {"PASE_QUEUE": "1"},                   # ready-queue claiming instead of the static order
 }
 
