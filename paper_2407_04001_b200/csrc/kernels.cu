@@ -1034,9 +1034,11 @@ __device__ __noinline__ void tile_stream_pf(const VertexDesc& vd, const TermDesc
             bulk_prefetch_l2((const void*)lo, (uint32_t)(hi - lo));
         }
     };
-    if (first < end && lane < V) prefetch_rows(first);
+    const int64_t ahead = (int64_t)vd.pf_ahead * stride;
+    for (int64_t k = 0; k < ahead; k += stride)
+        if (first + k < end && lane < V) prefetch_rows(first + k);
     for (int64_t item = first; item < end; item += stride) {
-        if (item + stride < end && lane < V) prefetch_rows(item + stride);
+        if (item + ahead < end && lane < V) prefetch_rows(item + ahead);
         int64_t obase;
         const double* pp[NP];
         const double* sp[NS];

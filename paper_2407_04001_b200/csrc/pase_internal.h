@@ -130,6 +130,7 @@ struct VertexDesc {          // one DP vertex (rank i)
     int32_t part;            // multi-GPU: table partitioned by its top coordinate
     int32_t psub;            // partitioned: combinations below the top coordinate (ncombo / K_top)
     int32_t bcast;           // bit 0: write T to every rank, bit 1: write A to every rank
+    int32_t pf_ahead;        // stream L2-prefetch form: items of lookahead (0 = the current item)
     int32_t npeer;           // peers written when bcast != 0 (world - 1)
     double* Tpeer[kMaxWorld - 1];     // this vertex's T / A in the peers' pools
     uint16_t* Apeer[kMaxWorld - 1];

@@ -40,6 +40,11 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     // ---- per (vertex, rank): unit runs, split into tasks
     struct GTask { int32_t rank, vtx; int64_t i0, i1; int32_t glog; };   // glog 0 = the vertex's
     std::vector<GTask> all;
+    {
+        int64_t est = 0;                                // reserve: ~ items / spread tasks per vertex
+        for (int i = 0; i < n; ++i) est += std::min<int64_t>(spread, 1 + (vd[i].shape >= 0 ? vd[i].nitems : vd[i].nout) / 64);
+        all.reserve((size_t)(est * G + 16));
+    }
     // tasks_of[i] for DP vertex i; tasks_of[n + i] = the cost-table chunks vertex i reads (run by
     // every rank: each needs the full L / W tables), which its tasks wait for like children
     const int nv = chunk_consumer ? 2 * n : n;
@@ -154,6 +159,8 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     for (int i = n; i < nv; ++i) bl[i] = 4.0 + bl[i - n];
     const auto tt1 = std::chrono::steady_clock::now();
     std::vector<double> start(ntk, -1.0);
+    std::vector<int32_t> start_seq;                     // tasks in simulated start order
+    start_seq.reserve((size_t)ntk);
     if (!simulate) {
         // ready-queue claiming (single GPU): the order only ranks the leaves' tasks published at
         // the start -- critical path (bottom level) first; no list-schedule simulation
@@ -184,6 +191,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
                     const double d = tdur[run[cursor[vq]]];
                     int32_t k = 0;
                     while (k < free_w[q] && cursor[vq] < (int32_t)run.size() && tdur[run[cursor[vq]]] == d) {
+                        start_seq.push_back(run[cursor[vq]]);
                         start[run[cursor[vq]++]] = now;
                         ++k;
                     }
@@ -214,15 +222,23 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         }
     }
     const auto tt2 = std::chrono::steady_clock::now();
-    if (const char* tv = std::getenv("PASE_TIMING"); tv && tv[0] == '1')
-        std::fprintf(stderr, "[pase] schedule: tasks+pending %.3f ms, list-schedule %.3f ms (%lld tasks)\n",
-                     std::chrono::duration<double, std::milli>(tt1 - tt0).count(),
-                     std::chrono::duration<double, std::milli>(tt2 - tt1).count(), (long long)ntk);
     // ---- this rank's tasks in simulated start order
     std::vector<int32_t> mine;
-    for (int64_t t = 0; t < ntk; ++t)
-        if (all[t].rank == rank) mine.push_back((int32_t)t);
-    std::stable_sort(mine.begin(), mine.end(), [&](int32_t a, int32_t b) { return start[a] < start[b]; });
+    mine.reserve((size_t)ntk);
+    if (simulate) {                                     // start order; equal start times by task id
+        for (int32_t t : start_seq)
+            if (all[t].rank == rank) mine.push_back(t);
+        for (size_t a = 0; a < mine.size();) {
+            size_t b = a + 1;
+            while (b < mine.size() && start[mine[b]] == start[mine[a]]) ++b;
+            if (b - a > 1) std::sort(mine.begin() + a, mine.begin() + b);
+            a = b;
+        }
+    } else {
+        for (int64_t t = 0; t < ntk; ++t)
+            if (all[t].rank == rank) mine.push_back((int32_t)t);
+        std::stable_sort(mine.begin(), mine.end(), [&](int32_t a, int32_t b) { return start[a] < start[b]; });
+    }
     out.tasks.clear();
     out.order.clear();
     std::vector<int32_t> local_id(ntk, -1);       // local ids in vertex order
@@ -244,6 +260,12 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     for (int32_t t : out.order)
         if (out.tasks[t].vtx >= 0 && out.pending[out.tasks[t].vtx] == 0) out.ready0.push_back(t);
     out.total_tasks = ntk;
+    if (const char* tv = std::getenv("PASE_TIMING"); tv && tv[0] == '1')
+        std::fprintf(stderr, "[pase] schedule: tasks+pending %.3f ms, list-schedule %.3f ms, order %.3f ms (%lld tasks)\n",
+                     std::chrono::duration<double, std::milli>(tt1 - tt0).count(),
+                     std::chrono::duration<double, std::milli>(tt2 - tt1).count(),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tt2).count(),
+                     (long long)ntk);
     return PASE_OK;
 }
 

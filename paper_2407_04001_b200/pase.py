@@ -219,6 +219,7 @@ class Graph:
     def __init__(self, graph: dict):
         self.graph = graph
         self.c_graph, self._keep = marshal_graph(graph)
+        self.n_dims = [len(nd["dims"]) for nd in graph["nodes"]]
 
 
 def make_machine(flops: float = 1e13, bandwidth: float = 1e10, policy: int = PASE_CFG_EXACT_P,
@@ -258,6 +259,7 @@ class Context:
             g, self._keep = marshal_graph(graph)
         self.graph = graph
         self.n, self.m, self.p = len(graph["nodes"]), len(graph["edges"]), int(p)
+        self._nd = G.n_dims if G is not None else [len(nd["dims"]) for nd in graph["nodes"]]
         order = ORDERINGS[ordering] if isinstance(ordering, str) else int(ordering)
         self._mach = make_machine(flops, bandwidth, pol, device, stream, rank, world, virtual_ranks,
                                   table_budget, redundant_below, order)
@@ -296,7 +298,7 @@ class Context:
         idx = np.zeros(self.n, np.int32)
         tot = C.c_double()
         self._chk(self._L.pase_solve(self._h, _ptr(cfg, C.c_int32), _ptr(idx, C.c_int32), C.byref(tot)))
-        tuples = [tuple(int(c) for c in cfg[v, :len(self.graph["nodes"][v]["dims"])]) for v in range(self.n)]
+        tuples = [tuple(r[:d]) for r, d in zip(cfg.tolist(), self._nd)]
         return {"cost": tot.value, "config_index": idx, "configs": tuples}
 
     # ---- row f2: Eq. 1 on the GPU
@@ -339,7 +341,7 @@ class Context:
         idx = np.zeros(self.n, np.int32)
         tot = C.c_double()
         self._chk(self._L.pase_finish(self._h, _ptr(cfg, C.c_int32), _ptr(idx, C.c_int32), C.byref(tot)))
-        tuples = [tuple(int(c) for c in cfg[v, :len(self.graph["nodes"][v]["dims"])]) for v in range(self.n)]
+        tuples = [tuple(r[:d]) for r, d in zip(cfg.tolist(), self._nd)]
         return {"cost": tot.value, "config_index": idx, "configs": tuples}
 
     def export_handle(self) -> bytes:
