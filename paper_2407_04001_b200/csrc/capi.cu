@@ -620,7 +620,7 @@ pase_status prepare(pase_ctx* ctx, bool device) {
                 // its rows staged into shared memory by TMA bulk copies
                 if (last_spans && NS >= 1 && stream_tma() == 1) d.shape = pase::kShapeStream + (NP - 1) * 4 + NS;
                 if (last_spans && NS >= 1 && stream_tma() == 2) d.shape = pase::kShapeStreamPF + (NP - 1) * 4 + NS;
-                static const int ahead = std::getenv("PASE_STREAM_PF_AHEAD") ? std::atoi(std::getenv("PASE_STREAM_PF_AHEAD")) : 1;
+                static const int ahead = std::getenv("PASE_STREAM_PF_AHEAD") ? std::atoi(std::getenv("PASE_STREAM_PF_AHEAD")) : 0;
                 d.pf_ahead = ahead;
             } else if (d.wlog == 0 && d.K <= 3) {             // one lane per item
                 d.glog = 0;
