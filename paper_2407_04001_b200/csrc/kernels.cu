@@ -1358,7 +1358,7 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
             continue;
         }
         if (tk.vtx != cur) {                                // descriptors: static, fetch now
-            if (threadIdx.x == 0) vd = vds[tk.vtx];
+            stage_struct(&vd, vds + tk.vtx);                // one 4-B word per thread: one round of loads
             __syncthreads();
             const int nt = min(vd.nterms, kMaxTermsSh);
             for (int k = threadIdx.x; k < nt; k += blockDim.x) td[k] = tds[vd.term0 + k];
