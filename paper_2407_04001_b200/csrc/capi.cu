@@ -308,8 +308,10 @@ void widen_critical(pase_ctx* ctx) {
     }
 }
 
-// single-suffix 2-D tile only for vertices with at least this many candidates
-const int64_t kMin2S = std::getenv("PASE_MIN_2S") ? std::atoll(std::getenv("PASE_MIN_2S")) : (int64_t(1) << 24);
+// single-suffix 2-D tile only for vertices with at least this many candidates (round 2 sweep,
+// profiles/r02_ab_tiles.txt: 2^22 instead of 2^24 cuts the north-star DP 8 %, LE_P 1.4 %, neutral
+// on InceptionV3 / GNMT / RNNLM; 2^18 hurts InceptionV3 and GNMT)
+const int64_t kMin2S = std::getenv("PASE_MIN_2S") ? std::atoll(std::getenv("PASE_MIN_2S")) : (int64_t(1) << 22);
 
 void set_tile2(VertexDesc& d, int q2, int f2) {
     d.q2 = q2;
