@@ -395,6 +395,13 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
     d.shape = pase::kShape2D + (NS - 1) * 4 + (d.glog - 2);
 }
 
+// dependency wait at each warp's tile gate, after its work-item decode (PASE_EARLY_GATE=0: one
+// thread per CTA waits before the tile starts)
+bool early_gate() {
+    static const bool on = !(std::getenv("PASE_EARLY_GATE") && std::getenv("PASE_EARLY_GATE")[0] == '0');
+    return on;
+}
+
 // streaming-vertex form (PASE_STREAM_TMA): 0 = direct full-warp loads, 1 = rows TMA-staged in a
 // shared-memory ring, 2 = direct loads with the next item's rows TMA-prefetched into L2
 int stream_tma() {
@@ -812,7 +819,7 @@ pase_status issue_schedule(pase_ctx* ctx, bool capture) {
         pase::launch_dp_persistent(ctx->d_vd, ctx->d_td, ctx->d_tasks, ctx->d_order, ctx->ntasks, ctx->d_sched,
                                    d_err, ctx->peers, cost_args(ctx), ctx->nblocks,
                                    trace_on() ? ctx->d_trace : nullptr, ctx->timeout_ns, ctx->stream_tiles,
-                                   ctx->d_ring, ctx->d_ring_tail, s);
+                                   ctx->d_ring, ctx->d_ring_tail, early_gate(), s);
         if (ctx->world > 1) pase::launch_rank_barrier(ctx->peers, ctx->d_bar, d_err, ctx->timeout_ns, s);
     } else {
         CUDA_TRY(cudaEventRecord(start, s));

@@ -275,6 +275,45 @@ __device__ __forceinline__ void st_out(const VertexDesc& vd, int64_t phi, double
         }
 }
 
+// Dependency gate of a persistent task (round 2): the task's vertex may only READ its child tables
+// once every child task has released them (pending counter = 0).  Each warp waits at its gate
+// right before its first table load -- after its work-item decode and pointer setup, which need
+// only the static descriptors -- so that setup overlaps the wait on the critical chain.  Lane 0
+// polls (relaxed, .gpu or .sys scope), then fences (the acquire pattern), then __syncwarp orders
+// the other lanes' loads after it.  A wait past the timeout flags the solve as failed (its
+// results are discarded) and lets the warp run on.
+struct Gate {
+    const int32_t* p;            // the vertex's pending counter; nullptr: nothing to wait for
+    int32_t* err;
+    uint64_t timeout_ns;
+    int multi;                   // group contexts: system scope (peers decrement it over NVLink)
+};
+__device__ __forceinline__ uint64_t gate_clock() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ int gate_poll(const int32_t* p, int multi) {
+    int v;
+    if (multi) asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    else asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void gate_wait(Gate& g) {
+    if (!g.p) return;
+    if ((threadIdx.x & 31) == 0 && gate_poll(g.p, g.multi) != 0) {
+        const uint64_t t0 = gate_clock();
+        while (gate_poll(g.p, g.multi) != 0)
+            if (g.timeout_ns && gate_clock() - t0 > g.timeout_ns) { atomicExch(g.err, 1); break; }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (g.multi) { int v; asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(g.p) : "memory"); (void)v; }
+        else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    __syncwarp();
+    g.p = nullptr;
+}
+
 // Items of [i0, i1) for the calling warp.  Throughput mode (wlog == 0): the warp's lane
 // groups take items first + k*stride + sub (warp-uniform loop).  Latency mode (G == 32,
 // W = 2^wlog warps per item, for small vertices on the critical path): the W warps of an item
@@ -282,7 +321,7 @@ __device__ __forceinline__ void st_out(const VertexDesc& vd, int64_t phi, double
 // minima are combined through shared memory (CTA-uniform loop, CTA barriers).
 template <int NP, int NS, int G>
 __device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td, int64_t first,
-                                        int64_t stride, int64_t i1, double* red_b, int* red_c) {
+                                        int64_t stride, int64_t i1, double* red_b, int* red_c, Gate gate) {
     constexpr int V = kTile;
     constexpr int LG = Log2<G>::value, LV = Log2<V>::value;
     constexpr int S = LG < LV ? LG : LV;          // halving (reduce-scatter) steps
@@ -338,6 +377,7 @@ __device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td
         const int Kv = nb > 0 ? vd.K : 0;
         const int jmax = nb > 0 ? nb - 1 : 0;
         const int cstep = G << wlog;
+        gate_wait(gate);                                    // children complete (first item only)
 #pragma unroll kCUnroll
         for (int C = lane + (wsub << LG); C < Kv; C += cstep) {   // unrolled: 2 C in flight
             double pre = ld(pp[0] + C);                     // L[C] (term 0 is never in the suffix)
@@ -421,7 +461,7 @@ __device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td
 // optionally also q2) or NS = 2 (both S terms on qstar only).
 template <int NS, int G>
 __device__ __noinline__ void tile2_items(const VertexDesc& vd, const TermDesc* td, int64_t first,
-                                         int64_t stride, int64_t end) {
+                                         int64_t stride, int64_t end, Gate gate) {
     constexpr int V1 = kTile1, V2 = kTile2, V = V1 * V2;
     constexpr int LG = Log2<G>::value, LV = Log2<V>::value;
     constexpr int S = LG < LV ? LG : LV;
@@ -485,6 +525,7 @@ __device__ __noinline__ void tile2_items(const VertexDesc& vd, const TermDesc* t
         const int m1 = nb1 > 0 ? nb1 - 1 : 0, m2 = nb2 > 0 ? nb2 - 1 : 0;
         // every load of an iteration is unconditional (unused slots re-read a valid address), so
         // they issue together; only the adds are predicated on the vertex's segment sizes
+        gate_wait(gate);
 #pragma unroll 1
         for (int C = lane; C < Kv; C += G) {
             double a[kMaxP0];
@@ -592,7 +633,7 @@ __device__ __noinline__ void tile2_items(const VertexDesc& vd, const TermDesc* t
 // 8 NS for 8), every address a per-item row pointer advanced by induction.
 template <int NP0, int NB, int NS2, int G>
 __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* td, int64_t first,
-                                          int64_t stride, int64_t end) {
+                                          int64_t stride, int64_t end, Gate gate) {
     constexpr int V1 = kTile1, V2 = kTile2, V = V1 * V2;
     constexpr int LG = Log2<G>::value, LV = Log2<V>::value;
     constexpr int S = LG < LV ? LG : LV;
@@ -699,6 +740,7 @@ __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* 
                     if (cost < best[j]) { best[j] = cost; bestC[j] = C; }   // strict <: lowest C
                 }
         };
+        gate_wait(gate);
         int C = lane;
 #pragma unroll 1
         for (; C + G < Kv; C += 2 * G) {
@@ -762,7 +804,7 @@ __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* 
 // Generic path (any number of terms, 64-bit strides): one lane group per output phi,
 // offsets recomputed per candidate.  Outputs [first + k*stride + sub, ...) < end.
 __device__ __noinline__ void generic_items(const VertexDesc& vd, const TermDesc* __restrict__ tds, int glog,
-                                           int64_t first, int64_t stride, int64_t end) {
+                                           int64_t first, int64_t stride, int64_t end, Gate gate) {
     const int g = 1 << glog;
     const int lane = threadIdx.x & (g - 1);
     const int sub = (threadIdx.x & 31) >> glog;
@@ -774,6 +816,7 @@ __device__ __noinline__ void generic_items(const VertexDesc& vd, const TermDesc*
         for (int q = 0; q < vd.m; ++q) { c[q] = (int32_t)(rem % vd.radix[q]); rem /= vd.radix[q]; }
         double best = __longlong_as_double(0x7ff0000000000000ll);
         int bestC = 0x7fffffff;
+        gate_wait(gate);
         for (int C = lane; C < K; C += g) {
             double cost = 0.0;
             for (int t = 0; t < vd.nterms; ++t) {
@@ -882,7 +925,8 @@ __device__ __forceinline__ void stream_decode(const VertexDesc& vd, const TermDe
 
 template <int NP, int NS>
 __device__ __noinline__ uint32_t tile_stream_items(const VertexDesc& vd, const TermDesc* td, int64_t first,
-                                                   int64_t stride, int64_t end, unsigned char* dyn, uint32_t seq) {
+                                                   int64_t stride, int64_t end, unsigned char* dyn, uint32_t seq,
+                                                   Gate gate) {
     constexpr int V = kTile, S = 3, H = 1;               // G = 32: 3 halving steps, then 2 more
     const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & (kStreamWarps - 1);
     double* buf = stream_buf(dyn, w);
@@ -907,6 +951,7 @@ __device__ __noinline__ uint32_t tile_stream_items(const VertexDesc& vd, const T
         return sp_[NS - 1] + (int64_t)min(lane, nb - 1) * sqs;
     };
     if (pitem < end && lane < V) prow = prow_of(pitem);
+    gate_wait(gate);
     if (lane < V) fence_proxy_async_global();            // acquired child writes -> async-proxy reads
     uint32_t pseq = seq;
     auto produce = [&]() {                               // stage chunk (pitem, pch) as sequence pseq
@@ -1012,7 +1057,7 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) 
 
 template <int NP, int NS>
 __device__ __noinline__ void tile_stream_pf(const VertexDesc& vd, const TermDesc* td, int64_t first,
-                                            int64_t stride, int64_t end) {
+                                            int64_t stride, int64_t end, Gate gate) {
     constexpr int V = kTile, S = 3;
     const int lane = threadIdx.x & 31;
     const int q = vd.qstar;
@@ -1049,6 +1094,7 @@ __device__ __noinline__ void tile_stream_pf(const VertexDesc& vd, const TermDesc
         int bestC[V];
 #pragma unroll
         for (int j = 0; j < V; ++j) { best[j] = __longlong_as_double(0x7ff0000000000000ll); bestC[j] = 0x7fffffff; }
+        gate_wait(gate);
 #pragma unroll 2
         for (int C = lane; C < K; C += 32) {
             double pre = ld(pp[0] + C);
@@ -1102,16 +1148,16 @@ __device__ __noinline__ void tile_stream_pf(const VertexDesc& vd, const TermDesc
 __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const TermDesc* td_sh,
                                           const TermDesc* tds_g, int64_t first_warp, int64_t nwarps,
                                           int64_t i0, int64_t i1, double* red_b, int* red_c,
-                                          unsigned char* dyn, uint32_t& seq) {
+                                          unsigned char* dyn, uint32_t& seq, Gate gate) {
     switch (shape) {
 #define PASE_CASE(NP, NS, LGG)                                                                    \
     case (NP - 1) * 16 + NS * 4 + (LGG - 2): {                                                    \
         constexpr int G_ = 1 << LGG, GPW_ = 32 / G_;                                              \
         if (G_ == 32 && vd.wlog)                                                                  \
             tile_items<NP, NS, G_>(vd, td_sh, i0 + (first_warp >> vd.wlog), nwarps >> vd.wlog, i1,   \
-                                   red_b, red_c);                                                 \
+                                   red_b, red_c, gate);                                           \
         else                                                                                      \
-            tile_items<NP, NS, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1, red_b, red_c); \
+            tile_items<NP, NS, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1, red_b, red_c, gate); \
         return;                                                                                   \
     }
 #define PASE_NS(NP, NS) PASE_CASE(NP, NS, 2) PASE_CASE(NP, NS, 3) PASE_CASE(NP, NS, 4) PASE_CASE(NP, NS, 5)
@@ -1124,7 +1170,7 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
         // thread, consecutive threads on consecutive items -- every store is a coalesced warp row
 #define PASE_CASE1(NP, NS)                                                                        \
     case kShapeG1 + (NP - 1) * 4 + NS:                                                            \
-        tile_items<NP, NS, 1>(vd, td_sh, i0 + first_warp * 32, nwarps * 32, i1, red_b, red_c);    \
+        tile_items<NP, NS, 1>(vd, td_sh, i0 + first_warp * 32, nwarps * 32, i1, red_b, red_c, gate); \
         return;
 #define PASE_NP1(NP) PASE_CASE1(NP, 0) PASE_CASE1(NP, 1) PASE_CASE1(NP, 2) PASE_CASE1(NP, 3)
         PASE_NP1(1) PASE_NP1(2) PASE_NP1(3) PASE_NP1(4)
@@ -1133,7 +1179,7 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
         // streaming regime: the spanning term staged by TMA bulk copies (one item per warp)
 #define PASE_CASES(NP, NS)                                                                        \
     case kShapeStream + (NP - 1) * 4 + NS:                                                        \
-        seq = tile_stream_items<NP, NS>(vd, td_sh, i0 + first_warp, nwarps, i1, dyn, seq);        \
+        seq = tile_stream_items<NP, NS>(vd, td_sh, i0 + first_warp, nwarps, i1, dyn, seq, gate);  \
         return;
 #define PASE_NPS(NP) PASE_CASES(NP, 1) PASE_CASES(NP, 2) PASE_CASES(NP, 3)
         PASE_NPS(1) PASE_NPS(2) PASE_NPS(3) PASE_NPS(4)
@@ -1142,7 +1188,7 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
         // streaming regime: direct coalesced loads, the next item's rows bulk-prefetched into L2
 #define PASE_CASEP(NP, NS)                                                                        \
     case kShapeStreamPF + (NP - 1) * 4 + NS:                                                      \
-        tile_stream_pf<NP, NS>(vd, td_sh, i0 + first_warp, nwarps, i1);                           \
+        tile_stream_pf<NP, NS>(vd, td_sh, i0 + first_warp, nwarps, i1, gate);                     \
         return;
 #define PASE_NPP(NP) PASE_CASEP(NP, 1) PASE_CASEP(NP, 2) PASE_CASEP(NP, 3)
         PASE_NPP(1) PASE_NPP(2) PASE_NPP(3) PASE_NPP(4)
@@ -1151,7 +1197,7 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
 #define PASE_CASE2(NS, LGG)                                                                       \
     case kShape2D + (NS - 1) * 4 + (LGG - 2): {                                                   \
         constexpr int G_ = 1 << LGG, GPW_ = 32 / G_;                                              \
-        tile2_items<NS, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1);                \
+        tile2_items<NS, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1, gate);          \
         return;                                                                                   \
     }
         PASE_CASE2(1, 2) PASE_CASE2(1, 3) PASE_CASE2(1, 4) PASE_CASE2(1, 5)
@@ -1160,7 +1206,7 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
 #define PASE_CASE2S(NP0, FORM, NB, NS2, LGG)                                                      \
     case kShape2S + ((NP0 - 1) * 4 + FORM) * 4 + (LGG - 2): {                                     \
         constexpr int G_ = 1 << LGG, GPW_ = 32 / G_;                                              \
-        tile2s_items<NP0, NB, NS2, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1);     \
+        tile2s_items<NP0, NB, NS2, G_>(vd, td_sh, i0 + first_warp * GPW_, nwarps * GPW_, i1, gate); \
         return;                                                                                   \
     }
 #define PASE_2S_G(NP0, FORM, NB, NS2)                                                             \
@@ -1174,7 +1220,7 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
 #undef PASE_CASE2S
         default: {
             const int gpw = 32 >> vd.glog;
-            generic_items(vd, tds_g, vd.glog, i0 + first_warp * gpw, nwarps * gpw, i1);
+            generic_items(vd, tds_g, vd.glog, i0 + first_warp * gpw, nwarps * gpw, i1, gate);
         }
     }
 }
@@ -1195,7 +1241,8 @@ dp_fill_vertex(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ 
     uint32_t seq = 0;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    run_shape(vd.shape, vd, td, tds, warp, nwarps, 0, vd.shape >= 0 ? vd.nitems : vd.nout, red_b, red_c, dyn, seq);
+    run_shape(vd.shape, vd, td, tds, warp, nwarps, 0, vd.shape >= 0 ? vd.nitems : vd.nout, red_b, red_c, dyn, seq,
+              Gate{nullptr, nullptr, 0, 0});
 }
 
 void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vertex,
@@ -1291,7 +1338,7 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
               const TaskDesc* __restrict__ tasks, const int32_t* __restrict__ order, int ntasks,
               int32_t* __restrict__ sched, int32_t* __restrict__ err, Peers peers, CostArgs cost,
               int64_t* __restrict__ trace, uint64_t timeout_ns, int stream_smem, int32_t* __restrict__ ring,
-              int32_t* __restrict__ ring_tail) {
+              int32_t* __restrict__ ring_tail, int early_gate) {
     // sched: [0] claim counter / ring head (own 128-B line), [kSchedLine, +n) pending per vertex
     int32_t* head = sched;
     int32_t* pending = sched + kSchedLine;
@@ -1364,8 +1411,10 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
             for (int k = threadIdx.x; k < nt; k += blockDim.x) td[k] = tds[vd.term0 + k];
             cur = tk.vtx;
         }
-        if (queue) {
-            // ready by construction; TMA reads of the children need the proxy fence (tile entry)
+        if (queue || early_gate) {
+            // queue: ready by construction.  early gate: every warp waits at its tile's gate,
+            // after its work-item decode (the gate fences; the stream tiles add the proxy fence)
+            if (early_gate && trace && threadIdx.x == 0) t_start = (int64_t)globaltimer();
         } else if (threadIdx.x == 0) {                      // wait for the children's tasks
             int32_t* pv = pending + tk.vtx;
             if ((multi ? ld_relaxed_sys(pv) : ld_relaxed(pv)) != 0) {
@@ -1393,7 +1442,8 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
         // wave-tail tasks (schedule.cpp) run the vertex's tile with wider lane groups: every
         // tile family encodes log2(G) - 2 in the shape's low 2 bits
         const int shape = tk.glog ? ((vd.shape & ~3) | (tk.glog - 2)) : vd.shape;
-        run_shape(shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1, red_b, red_c, dyn, seq);
+        const Gate gate{(early_gate && !queue) ? pending + tk.vtx : nullptr, err, timeout_ns, multi ? 1 : 0};
+        run_shape(shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1, red_b, red_c, dyn, seq, gate);
         int64_t t_comp = 0, t_sync = 0;
         if (trace && threadIdx.x == 0) t_comp = (int64_t)globaltimer();
         __syncthreads();                                    // task's stores precede the release
@@ -1453,12 +1503,12 @@ void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, cons
                           const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
                           const Peers& peers, const CostArgs& cost, int nblocks, int64_t* trace_dev,
                           uint64_t timeout_ns, bool stream_tiles, int32_t* ring, int32_t* ring_tail,
-                          void* stream) {
+                          bool early_gate, void* stream) {
     const size_t dyn = stream_tiles ? kStreamSmemBytes : 0;
     dp_persistent<<<(unsigned)nblocks, 256, dyn, (cudaStream_t)stream>>>(vd_dev, td_dev, tasks_dev, order_dev,
                                                                            ntasks, sched_dev, err_dev, peers,
                                                                            cost, trace_dev, timeout_ns, (int)dyn,
-                                                                           ring, ring_tail);
+                                                                           ring, ring_tail, early_gate ? 1 : 0);
 }
 
 // Group barrier between the ranks of a multi-GPU search (before and after the DP): every

@@ -182,7 +182,10 @@ __host__ __device__
 constexpr bool stream_smem_shape(int s) { return s >= kShapeStream && s < kShapeStreamPF; }
 //   form 0: P1 = [A], S = [S1]; 1: P1 = [A, B], S = [S1]; 2: S = [S1, const]; 3: S = [S1, S2 on q1]
 constexpr int kMaxP0 = 4, kMaxP1 = 2;   // 2-D tile: max scalar-prefix / q2-prefix terms
-constexpr int kCostRows = 64;  // edge-table rows per cost-table CTA
+#ifndef PASE_COST_ROWS
+#define PASE_COST_ROWS 64
+#endif
+constexpr int kCostRows = PASE_COST_ROWS;  // edge-table rows per cost-table CTA
 constexpr int kCostCols = 512; // edge-table columns staged per pass
 
 struct CostArgs {            // the cost-table computation (kernel parameter)
@@ -238,7 +241,7 @@ void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, cons
                           const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
                           const Peers& peers, const CostArgs& cost, int nblocks, int64_t* trace_dev,
                           uint64_t timeout_ns, bool stream_tiles, int32_t* ring, int32_t* ring_tail,
-                          void* stream);
+                          bool early_gate, void* stream);
 void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev, uint64_t timeout_ns, void* stream);
 int persistent_blocks_per_sm();
 void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,

@@ -22,6 +22,7 @@ VARIANTS = {
     "streaming_smem_ring": {"PASE_STREAM_MB": "0", "PASE_STREAM_TMA": "1"},  # ... TMA smem ring
     "streaming_no_tma": {"PASE_STREAM_MB": "0", "PASE_STREAM_TMA": "0"},   # ... or plain full-warp 1-D tile
     "ready_queue": {"PASE_QUEUE": "1"},                   # ready-queue claiming instead of the static order
+    "cta_gate": {"PASE_EARLY_GATE": "0"},                 # one thread per CTA waits before the tile
 }
 
 
