@@ -35,7 +35,8 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     const int n = P.n;
     const int G = std::max(world, 1);
     nblocks = std::max(nblocks, 1);
-    const int64_t spread = (int64_t)kTasksPerBlock * nblocks;
+    static const int64_t tpb = std::getenv("PASE_TASKS_PER_BLOCK") ? std::atoll(std::getenv("PASE_TASKS_PER_BLOCK")) : kTasksPerBlock;
+    const int64_t spread = std::max<int64_t>(1, tpb) * nblocks;
     const auto tt0 = std::chrono::steady_clock::now();
     // ---- per (vertex, rank): unit runs, split into tasks
     struct GTask { int32_t rank, vtx; int64_t i0, i1; int32_t glog; };   // glog 0 = the vertex's
@@ -48,7 +49,19 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     // tasks_of[i] for DP vertex i; tasks_of[n + i] = the cost-table chunks vertex i reads (run by
     // every rank: each needs the full L / W tables), which its tasks wait for like children
     const int nv = chunk_consumer ? 2 * n : n;
-    std::vector<std::vector<std::vector<int32_t>>> tasks_of(nv, std::vector<std::vector<int32_t>>(G));
+    // (vertex, rank) -> its tasks: a counting sort of `all` by vtx * G + rank after it is built
+    // (no per-vertex vectors: the host plan is on the end-to-end path)
+    std::vector<int32_t> toff((size_t)nv * G + 1, 0), tidx;
+    struct Span {
+        const int32_t* b;
+        const int32_t* e;
+        const int32_t* begin() const { return b; }
+        const int32_t* end() const { return e; }
+        size_t size() const { return (size_t)(e - b); }
+        bool empty() const { return b == e; }
+        int32_t operator[](size_t k) const { return b[k]; }
+    };
+    auto tasks_of = [&](int v, int q) { return Span{tidx.data() + toff[(size_t)v * G + q], tidx.data() + toff[(size_t)v * G + q + 1]}; };
     for (int i = 0; i < n; ++i) {
         const VertexDesc& d = vd[i];
         const int64_t units = d.shape >= 0 ? d.nitems : d.nout;
@@ -94,7 +107,6 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
                 for (int64_t a = r.first; a < r.second;) {
                     const bool tail = bulk_end >= 0 && a >= bulk_end;
                     const int64_t len = tail ? (256 >> tail_glog) : ti;
-                    tasks_of[i][q].push_back((int32_t)all.size());
                     all.push_back({q, i, a, std::min(r.second, a + len), tail ? tail_glog : 0});
                     a += len;
                 }
@@ -103,9 +115,15 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     if (chunk_consumer)
         for (int c = 0; c < (int)chunk_consumer->size(); ++c)
             for (int q = 0; q < G; ++q) {
-                tasks_of[n + (*chunk_consumer)[c]][q].push_back((int32_t)all.size());
                 all.push_back({q, n + (*chunk_consumer)[c], c, c + 1, 0});
             }
+    for (const GTask& t : all) ++toff[(size_t)t.vtx * G + t.rank + 1];
+    for (size_t k = 1; k < toff.size(); ++k) toff[k] += toff[k - 1];
+    tidx.resize(all.size());
+    {
+        std::vector<int32_t> fill(toff.begin(), toff.end() - 1);
+        for (size_t t = 0; t < all.size(); ++t) tidx[fill[(size_t)all[t].vtx * G + all[t].rank]++] = (int32_t)t;
+    }
     // ---- broadcast flags (bit 0: T, bit 1: A)
     for (int j = 0; j < n; ++j) {
         VertexDesc& d = vd[j];
@@ -124,15 +142,15 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         int64_t s = 0;
         for (int j : P.children[p]) {
             if (vd[j].bcast & 1)
-                for (int r = 0; r < G; ++r) s += (int64_t)tasks_of[j][r].size();
+                for (int r = 0; r < G; ++r) s += (int64_t)tasks_of(j, r).size();
             else
-                s += (int64_t)tasks_of[j][q].size();
+                s += (int64_t)tasks_of(j, q).size();
         }
         return s;
     };
     std::vector<std::vector<int64_t>> pend(G, std::vector<int64_t>(n));
     for (int q = 0; q < G; ++q)
-        for (int p = 0; p < n; ++p) pend[q][p] = waits_on(p, q) + (nv > n ? (int64_t)tasks_of[n + p][q].size() : 0);
+        for (int p = 0; p < n; ++p) pend[q][p] = waits_on(p, q) + (nv > n ? (int64_t)tasks_of(n + p, q).size() : 0);
     out.pending.assign(n, 0);
     for (int p = 0; p < n; ++p) {
         if (pend[rank][p] > INT32_MAX) { err = "internal: pending counter overflow"; return PASE_ERR_RESOURCE; }
@@ -152,7 +170,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     for (int i = n - 1; i >= 0; --i) {                 // parents have higher ranks
         double work = 0.0, longest = 0.0;
         for (int q = 0; q < G; ++q)
-            for (int32_t t : tasks_of[i][q]) { work += tdur[t]; longest = std::max(longest, tdur[t]); }
+            for (int32_t t : tasks_of(i, q)) { work += tdur[t]; longest = std::max(longest, tdur[t]); }
         const double vt = std::max(longest, work / ((double)nblocks * G));
         bl[i] = vt + (P.parent[i] >= 0 ? bl[P.parent[i]] : 0.0);
     }
@@ -175,7 +193,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         struct EV { double t; int32_t vq, k; bool operator>(const EV& o) const { return t != o.t ? t > o.t : vq > o.vq; } };
         std::priority_queue<EV, std::vector<EV>, std::greater<EV>> events;
         auto release = [&](int v, int q) {
-            if (!tasks_of[v][q].empty()) ready[q].push({bl[v], -(v * G + q)});
+            if (!tasks_of(v, q).empty()) ready[q].push({bl[v], -(v * G + q)});
         };
         for (int i = 0; i < nv; ++i)
             for (int q = 0; q < G; ++q)
@@ -187,7 +205,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
             for (int q = 0; q < G; ++q)
                 while (free_w[q] > 0 && !ready[q].empty()) {
                     const int32_t vq = -ready[q].top().second;
-                    const auto& run = tasks_of[vq / G][q];
+                    const Span run = tasks_of(vq / G, q);
                     const double d = tdur[run[cursor[vq]]];
                     int32_t k = 0;
                     while (k < free_w[q] && cursor[vq] < (int32_t)run.size() && tdur[run[cursor[vq]]] == d) {
@@ -226,14 +244,8 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     std::vector<int32_t> mine;
     mine.reserve((size_t)ntk);
     if (simulate) {                                     // start order; equal start times by task id
-        for (int32_t t : start_seq)
+        for (int32_t t : start_seq)                    // ties: the simulation's priority order
             if (all[t].rank == rank) mine.push_back(t);
-        for (size_t a = 0; a < mine.size();) {
-            size_t b = a + 1;
-            while (b < mine.size() && start[mine[b]] == start[mine[a]]) ++b;
-            if (b - a > 1) std::sort(mine.begin() + a, mine.begin() + b);
-            a = b;
-        }
     } else {
         for (int64_t t = 0; t < ntk; ++t)
             if (all[t].rank == rank) mine.push_back((int32_t)t);
@@ -244,14 +256,14 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     std::vector<int32_t> local_id(ntk, -1);       // local ids in vertex order
     for (int i = 0; i < n; ++i) {
         vd[i].task0 = (int32_t)out.tasks.size();
-        for (int32_t t : tasks_of[i][rank]) {
+        for (int32_t t : tasks_of(i, rank)) {
             local_id[t] = (int32_t)out.tasks.size();
             out.tasks.push_back({i, all[t].glog, all[t].i0, all[t].i1});
         }
-        vd[i].ntasks = (int32_t)tasks_of[i][rank].size();
+        vd[i].ntasks = (int32_t)tasks_of(i, rank).size();
     }
     for (int i = n; i < nv; ++i)                        // cost-table tasks: vtx = -1 - chunk
-        for (int32_t t : tasks_of[i][rank]) {
+        for (int32_t t : tasks_of(i, rank)) {
             local_id[t] = (int32_t)out.tasks.size();
             out.tasks.push_back({(int32_t)(-1 - all[t].i0), 0, 0, 0});
         }
