@@ -196,9 +196,11 @@ int64_t pase_table_entries(const pase_ctx* ctx, int32_t rank);
 pase_status pase_set_cost_tables(pase_ctx* ctx, const double* L, const double* W);
 
 /* Persistent-schedule timeline (tracing; enabled by env PASE_TRACE=1 at pase_create): per DP
- * task of the last pase_solve, 6 int64 = {(smid << 32) | rank, t_claim_ns, t_start_ns (dependencies
- * met), t_computed_ns (warp 0 done), t_synced_ns (CTA done), t_end_ns (parent counter released)}
- * (%globaltimer).  Copies min(cap, n_tasks) records into out (may be NULL); returns n_tasks
+ * task of the last pase_solve, 22 int64 = {(smid << 32) | rank, t_claim_ns, t_start_ns (descriptors
+ * staged; dependencies met unless the early gate is on), t_computed_ns (warp 0 done), t_synced_ns
+ * (CTA done), t_end_ns (parent counter released)}, then per warp w = 0..7 {t_gate_seen_ns (the
+ * children's counter seen at zero), t_gate_fenced_ns (acquire fence done)} (0: the warp had no
+ * gate in this task) (%globaltimer).  Copies min(cap, n_tasks) records into out (may be NULL); returns n_tasks
  * (0 when tracing is off, -1 on a CUDA error). */
 int64_t pase_get_trace(const pase_ctx* ctx, int64_t* out, int64_t cap);
 

@@ -397,9 +397,21 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
 
 // dependency wait at each warp's tile gate, after its work-item decode (PASE_EARLY_GATE=0: one
 // thread per CTA waits before the tile starts)
-bool early_gate() {
-    static const bool on = !(std::getenv("PASE_EARLY_GATE") && std::getenv("PASE_EARLY_GATE")[0] == '0');
-    return on;
+// thread per CTA waits before the tile starts).  Bit 1 (PASE_WARM, default on): a task whose
+// children are still running when it is claimed runs its first work item once without stores
+// before the gate, so its tile's code is in this SM's instruction caches when the gate opens.
+// Bit 2 (PASE_GATE_ELECT=1): one warp per CTA polls the counter, the others a shared flag.
+// Bit 3 (PASE_CLAIM_AHEAD=1): a CTA claims its next task before releasing the current one.
+int early_gate() {
+    static const int mode = [] {
+        const char* e = std::getenv("PASE_EARLY_GATE");
+        if (e && e[0] == '0') return 0;
+        const char* w = std::getenv("PASE_WARM");
+        const char* el = std::getenv("PASE_GATE_ELECT");
+        const char* ca = std::getenv("PASE_CLAIM_AHEAD");
+        return ((w && w[0] == '0') ? 1 : 3) | ((el && el[0] == '1') ? 4 : 0) | ((ca && ca[0] == '1') ? 8 : 0);
+    }();
+    return mode;
 }
 
 // streaming-vertex form (PASE_STREAM_TMA): 0 = direct full-warp loads, 1 = rows TMA-staged in a

@@ -287,6 +287,15 @@ struct Gate {
     int32_t* err;
     uint64_t timeout_ns;
     int multi;                   // group contexts: system scope (peers decrement it over NVLink)
+    int* elect;                  // shared words {elected, open}: with non-null, the first warp to reach
+                                 // its gate polls the global counter and opens a shared flag the
+                                 // other warps spin on (one global poller per CTA instead of 8)
+    int64_t* stamp;              // PASE_TRACE: per-warp {counter seen at 0, fence done} (ns)
+    int warm;                    // CTA-uniform: the children were still running when the task was
+                                 // claimed -- run the first work item once WITHOUT stores before the
+                                 // gate (warms this SM's instruction caches with the tile's code
+                                 // path and its static rows; results discarded, L1 invalidated by
+                                 // the gate's fence)
 };
 __device__ __forceinline__ uint64_t gate_clock() {
     uint64_t t;
@@ -299,16 +308,35 @@ __device__ __forceinline__ int gate_poll(const int32_t* p, int multi) {
     else asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_shared_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_shared_relaxed(int* p, int v) {
+    asm volatile("st.relaxed.cta.shared.s32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
 __device__ __forceinline__ void gate_wait(Gate& g) {
     if (!g.p) return;
-    if ((threadIdx.x & 31) == 0 && gate_poll(g.p, g.multi) != 0) {
-        const uint64_t t0 = gate_clock();
-        while (gate_poll(g.p, g.multi) != 0)
-            if (g.timeout_ns && gate_clock() - t0 > g.timeout_ns) { atomicExch(g.err, 1); break; }
-    }
     if ((threadIdx.x & 31) == 0) {
+        // elected mode: the first warp here polls global memory, the others spin on the shared
+        // flag it opens after its acquire; each warp then fences itself (the poller's fence
+        // synchronises with the releases, a waiter's fence with the poller's flag store)
+        const bool poller = !g.elect || atomicCAS_block(g.elect, 0, 1) == 0;
+        if (poller) {
+            if (gate_poll(g.p, g.multi) != 0) {
+                const uint64_t t0 = gate_clock();
+                while (gate_poll(g.p, g.multi) != 0)
+                    if (g.timeout_ns && gate_clock() - t0 > g.timeout_ns) { atomicExch(g.err, 1); break; }
+            }
+        } else {
+            while (ld_shared_relaxed(g.elect + 1) == 0) __nanosleep(64);
+        }
+        if (g.stamp) g.stamp[2 * (threadIdx.x >> 5)] = (int64_t)gate_clock();
         if (g.multi) { int v; asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(g.p) : "memory"); (void)v; }
         else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (poller && g.elect) st_shared_relaxed(g.elect + 1, 1);
+        if (g.stamp) g.stamp[2 * (threadIdx.x >> 5) + 1] = (int64_t)gate_clock();
     }
     __syncwarp();
     g.p = nullptr;
@@ -338,8 +366,11 @@ __device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td
     const int64_t wib = (threadIdx.x >> 5) >> wlog;                // item slot within the CTA
     const int64_t b0 = wlog ? first - wib : first;
     const int64_t end = i1;
+    // warm pass (Gate::warm): the first round once without stores, then the live rounds; one
+    // loop body (live is loop-variant, so the body is not duplicated)
+    bool live = !(gate.warm && gate.p);
 
-    for (int64_t base = b0; base < end; base += stride) {
+    for (int64_t base = b0; base < end;) {
         const int64_t item = wlog ? base + wib : base + sub;
         const bool valid = item < end;
         const uint32_t it = valid ? (uint32_t)item : 0u;   // host guarantees nitems < 2^31
@@ -374,10 +405,10 @@ __device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td
         int bestC[V];
 #pragma unroll
         for (int j = 0; j < V; ++j) { best[j] = __longlong_as_double(0x7ff0000000000000ll); bestC[j] = 0x7fffffff; }
-        const int Kv = nb > 0 ? vd.K : 0;
+        const int Kv = nb > 0 ? (live ? vd.K : min(vd.K, kCUnroll * (G << wlog))) : 0;   // warm: one unrolled trip
         const int jmax = nb > 0 ? nb - 1 : 0;
         const int cstep = G << wlog;
-        gate_wait(gate);                                    // children complete (first item only)
+        if (live) gate_wait(gate);                          // children complete (first item only)
 #pragma unroll kCUnroll
         for (int C = lane + (wsub << LG); C < Kv; C += cstep) {   // unrolled: 2 C in flight
             double pre = ld(pp[0] + C);                     // L[C] (term 0 is never in the suffix)
@@ -436,16 +467,18 @@ __device__ __noinline__ void tile_items(const VertexDesc& vd, const TermDesc* td
                 double b = red_b[w * V + lane];
                 int c = red_c[w * V + lane];
                 for (int k = 1; k < (1 << wlog); ++k) combine(b, c, red_b[(w + k) * V + lane], red_c[(w + k) * V + lane]);
-                if (lane < nb) st_out(vd, obase + (int64_t)(x0 + lane) * vd.ostride_q, b, c);
+                if (live && lane < nb) st_out(vd, obase + (int64_t)(x0 + lane) * vd.ostride_q, b, c);
             }
             __syncthreads();
-        } else if ((lane & ((G >> S) - 1)) == 0) {
+        } else if (live && (lane & ((G >> S) - 1)) == 0) {
 #pragma unroll
             for (int k = 0; k < H; ++k) {
                 const int j = jbase + k;
                 if (j < nb) st_out(vd, obase + (int64_t)(x0 + j) * vd.ostride_q, best[k], bestC[k]);
             }
         }
+        if (live) base += stride;
+        live = true;
     }
 }
 
@@ -478,7 +511,8 @@ __device__ __noinline__ void tile2_items(const VertexDesc& vd, const TermDesc* t
 #pragma unroll
     for (int t = 0; t < NS; ++t) { s1[t] = (int)td[ts + t].stride[q1]; s2[t] = (int)td[ts + t].stride[q2]; }
 
-    for (int64_t base = first; base < end; base += stride) {
+    bool live = !(gate.warm && gate.p);                 // warm pass: see tile_items
+    for (int64_t base = first; base < end;) {
         const int64_t item = base + sub;
         const bool valid = item < end;
         const uint32_t it = valid ? (uint32_t)item : 0u;
@@ -521,11 +555,11 @@ __device__ __noinline__ void tile2_items(const VertexDesc& vd, const TermDesc* t
         int bestC[V];
 #pragma unroll
         for (int j = 0; j < V; ++j) { best[j] = __longlong_as_double(0x7ff0000000000000ll); bestC[j] = 0x7fffffff; }
-        const int Kv = (nb1 > 0 && nb2 > 0) ? vd.K : 0;
+        const int Kv = (nb1 > 0 && nb2 > 0) ? (live ? vd.K : min(vd.K, G)) : 0;   // warm: one trip
         const int m1 = nb1 > 0 ? nb1 - 1 : 0, m2 = nb2 > 0 ? nb2 - 1 : 0;
         // every load of an iteration is unconditional (unused slots re-read a valid address), so
         // they issue together; only the adds are predicated on the vertex's segment sizes
-        gate_wait(gate);
+        if (live) gate_wait(gate);
 #pragma unroll 1
         for (int C = lane; C < Kv; C += G) {
             double a[kMaxP0];
@@ -610,7 +644,7 @@ __device__ __noinline__ void tile2_items(const VertexDesc& vd, const TermDesc* t
 #pragma unroll
         for (int s = 0; s < S; ++s)
             if (lane & (G >> (s + 1))) jbase += V >> (s + 1);
-        if ((lane & ((G >> S) - 1)) == 0) {
+        if (live && (lane & ((G >> S) - 1)) == 0) {
 #pragma unroll
             for (int k = 0; k < H; ++k) {
                 const int j = jbase + k, j1 = j / V2, j2 = j % V2;
@@ -619,6 +653,8 @@ __device__ __noinline__ void tile2_items(const VertexDesc& vd, const TermDesc* t
                            best[k], bestC[k]);
             }
         }
+        if (live) base += stride;
+        live = true;
     }
 }
 
@@ -645,7 +681,8 @@ __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* 
     const int q1 = vd.qstar, q2 = vd.q2;
     const int64_t sb = td[TA].stride[q2], ss = td[TS].stride[q1];
     const int64_t ss2 = NS2 == 2 ? td[TS + 1].stride[q1] : 0;
-    for (int64_t base = first; base < end; base += stride) {
+    bool live = !(gate.warm && gate.p);                 // warm pass: see tile_items
+    for (int64_t base = first; base < end;) {
         const int64_t item = base + sub;
         const bool valid = item < end;
         const uint32_t it = valid ? (uint32_t)item : 0u;
@@ -705,7 +742,7 @@ __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* 
         int bestC[V];
 #pragma unroll
         for (int j = 0; j < V; ++j) { best[j] = __longlong_as_double(0x7ff0000000000000ll); bestC[j] = 0x7fffffff; }
-        const int Kv = (nb1 > 0 && nb2 > 0) ? vd.K : 0;
+        const int Kv = (nb1 > 0 && nb2 > 0) ? (live ? vd.K : min(vd.K, 2 * G)) : 0;   // warm: one trip
         // every row pointer starts at this lane's C and advances by 2G per double iteration;
         // the second iteration's loads carry +G as an immediate
         auto step = [&](auto off, int C) {
@@ -740,7 +777,7 @@ __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* 
                     if (cost < best[j]) { best[j] = cost; bestC[j] = C; }   // strict <: lowest C
                 }
         };
-        gate_wait(gate);
+        if (live) gate_wait(gate);
         int C = lane;
 #pragma unroll 1
         for (; C + G < Kv; C += 2 * G) {
@@ -789,7 +826,7 @@ __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* 
 #pragma unroll
         for (int st = 0; st < S; ++st)
             if (lane & (G >> (st + 1))) jbase += V >> (st + 1);
-        if ((lane & ((G >> S) - 1)) == 0) {
+        if (live && (lane & ((G >> S) - 1)) == 0) {
 #pragma unroll
             for (int k = 0; k < H; ++k) {
                 const int j = jbase + k, j1 = j / V2, j2 = j % V2;
@@ -798,6 +835,8 @@ __device__ __noinline__ void tile2s_items(const VertexDesc& vd, const TermDesc* 
                            best[k], bestC[k]);
             }
         }
+        if (live) base += stride;
+        live = true;
     }
 }
 
@@ -808,15 +847,16 @@ __device__ __noinline__ void generic_items(const VertexDesc& vd, const TermDesc*
     const int g = 1 << glog;
     const int lane = threadIdx.x & (g - 1);
     const int sub = (threadIdx.x & 31) >> glog;
-    for (int64_t base = first; base < end; base += stride) {
+    bool live = !(gate.warm && gate.p);                 // warm pass: see tile_items
+    for (int64_t base = first; base < end;) {
         const int64_t phi = base + sub;
-        const int K = phi < end ? vd.K : 0;
+        const int K = phi < end ? (live ? vd.K : min(vd.K, g)) : 0;   // warm: one trip
         int32_t c[kMaxDep];
         int64_t rem = phi < end ? phi : 0;
         for (int q = 0; q < vd.m; ++q) { c[q] = (int32_t)(rem % vd.radix[q]); rem /= vd.radix[q]; }
         double best = __longlong_as_double(0x7ff0000000000000ll);
         int bestC = 0x7fffffff;
-        gate_wait(gate);
+        if (live) gate_wait(gate);
         for (int C = lane; C < K; C += g) {
             double cost = 0.0;
             for (int t = 0; t < vd.nterms; ++t) {
@@ -833,7 +873,9 @@ __device__ __noinline__ void generic_items(const VertexDesc& vd, const TermDesc*
             const int oc = __shfl_xor_sync(0xffffffffu, bestC, o);
             combine(best, bestC, ob, oc);
         }
-        if (lane == 0 && K > 0) st_out(vd, phi, best, bestC);
+        if (live && lane == 0 && K > 0) st_out(vd, phi, best, bestC);
+        if (live) base += stride;
+        live = true;
     }
 }
 
@@ -1242,7 +1284,7 @@ dp_fill_vertex(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ 
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     run_shape(vd.shape, vd, td, tds, warp, nwarps, 0, vd.shape >= 0 ? vd.nitems : vd.nout, red_b, red_c, dyn, seq,
-              Gate{nullptr, nullptr, 0, 0});
+              Gate{nullptr, nullptr, 0, 0, nullptr, nullptr, 0});
 }
 
 void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vertex,
@@ -1350,6 +1392,16 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
     __shared__ double red_b[8 * kTile];                     // latency-mode partial minima
     __shared__ int red_c[8 * kTile];
     __shared__ int s_task;
+    __shared__ int s_warm;                                  // Gate::warm of the current task
+    __shared__ int s_elect[2];                              // Gate::elect of the current task
+    // claim-ahead (early_gate bit 3): thread 0 claims the NEXT task as soon as its own warp has
+    // finished the current tile, so the claim's atomic and order lookup overlap the other warps'
+    // tails, the CTA barrier and the release.  Deadlock-free like the plain claim: a CTA's
+    // pending next task is later in the (topological) order than its unfinished current one.
+    __shared__ int s_next;
+    const bool ahead = !queue && (early_gate & 8);
+    int64_t t_claim_next = 0;
+    if (threadIdx.x == 0) s_next = -2;                      // -2: nothing claimed ahead
     __shared__ CostSmem csm;                                // cost-table tasks
     extern __shared__ __align__(128) unsigned char dyn[];   // stream-tile rings (launched with them
     const bool stream = stream_smem != 0;                   // only when a vertex uses a stream shape)
@@ -1362,7 +1414,11 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
     if (ld_relaxed(err) != 0) return;
     for (;;) {
         int64_t t_claim = 0, t_start = 0;
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0 && s_next != -2) {            // claimed ahead by the previous task
+            s_task = s_next;
+            s_next = -2;
+            t_claim = t_claim_next;
+        } else if (threadIdx.x == 0) {
             if (trace) t_claim = (int64_t)globaltimer();
             const int s = atomicAdd(head, 1);
             if (!queue) {
@@ -1413,8 +1469,14 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
         }
         if (queue || early_gate) {
             // queue: ready by construction.  early gate: every warp waits at its tile's gate,
-            // after its work-item decode (the gate fences; the stream tiles add the proxy fence)
-            if (early_gate && trace && threadIdx.x == 0) t_start = (int64_t)globaltimer();
+            // after its work-item decode (the gate fences; the stream tiles add the proxy fence).
+            // early_gate bit 1: a task whose children still run warms its tile first (Gate::warm)
+            if (early_gate && threadIdx.x == 0) {
+                if (trace) t_start = (int64_t)globaltimer();
+                s_elect[0] = s_elect[1] = 0;
+                s_warm = !queue && (early_gate & 2) && !stream_smem_shape(vd.shape) &&
+                         (multi ? ld_relaxed_sys(pending + tk.vtx) : ld_relaxed(pending + tk.vtx)) != 0;
+            }
         } else if (threadIdx.x == 0) {                      // wait for the children's tasks
             int32_t* pv = pending + tk.vtx;
             if ((multi ? ld_relaxed_sys(pv) : ld_relaxed(pv)) != 0) {
@@ -1442,10 +1504,19 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
         // wave-tail tasks (schedule.cpp) run the vertex's tile with wider lane groups: every
         // tile family encodes log2(G) - 2 in the shape's low 2 bits
         const int shape = tk.glog ? ((vd.shape & ~3) | (tk.glog - 2)) : vd.shape;
-        const Gate gate{(early_gate && !queue) ? pending + tk.vtx : nullptr, err, timeout_ns, multi ? 1 : 0};
+        const Gate gate{(early_gate && !queue) ? pending + tk.vtx : nullptr, err, timeout_ns, multi ? 1 : 0,
+                        (early_gate & 4) ? s_elect : nullptr,
+                        trace ? trace + (int64_t)kTraceWords * task + kTraceTaskWords : nullptr,
+                        (early_gate && !queue) ? s_warm : 0};
+        if (gate.stamp && (threadIdx.x & 31) == 0) gate.stamp[2 * warp] = gate.stamp[2 * warp + 1] = 0;
         run_shape(shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1, red_b, red_c, dyn, seq, gate);
         int64_t t_comp = 0, t_sync = 0;
         if (trace && threadIdx.x == 0) t_comp = (int64_t)globaltimer();
+        if (ahead && threadIdx.x == 0) {
+            if (trace) t_claim_next = (int64_t)globaltimer();
+            const int s = atomicAdd(head, 1);
+            s_next = s < ntasks ? order[s] : -1;
+        }
         __syncthreads();                                    // task's stores precede the release
         if (queue) {
             if (threadIdx.x == 0) {
@@ -1503,12 +1574,12 @@ void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, cons
                           const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
                           const Peers& peers, const CostArgs& cost, int nblocks, int64_t* trace_dev,
                           uint64_t timeout_ns, bool stream_tiles, int32_t* ring, int32_t* ring_tail,
-                          bool early_gate, void* stream) {
+                          int early_gate, void* stream) {
     const size_t dyn = stream_tiles ? kStreamSmemBytes : 0;
     dp_persistent<<<(unsigned)nblocks, 256, dyn, (cudaStream_t)stream>>>(vd_dev, td_dev, tasks_dev, order_dev,
                                                                            ntasks, sched_dev, err_dev, peers,
                                                                            cost, trace_dev, timeout_ns, (int)dyn,
-                                                                           ring, ring_tail, early_gate ? 1 : 0);
+                                                                           ring, ring_tail, early_gate);
 }
 
 // Group barrier between the ranks of a multi-GPU search (before and after the DP): every

@@ -150,7 +150,8 @@ struct Peers {               // kernel parameter: the group's scheduler words (d
     int32_t world, rank;
 };
 
-constexpr int kTraceWords = 6;                // PASE_TRACE record per task (pase_get_trace)
+constexpr int kTraceTaskWords = 6;            // PASE_TRACE record per task (pase_get_trace) ...
+constexpr int kTraceWords = kTraceTaskWords + 2 * 8;   // ... + per warp {gate seen, gate fenced}
 constexpr int kTasksPerBlock = 4;   // big vertices: ~4 tasks per CTA of the grid
 
 struct SchedPlan {           // build_schedule output for one rank
@@ -241,7 +242,7 @@ void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, cons
                           const int32_t* order_dev, int ntasks, int32_t* sched_dev, int32_t* err_dev,
                           const Peers& peers, const CostArgs& cost, int nblocks, int64_t* trace_dev,
                           uint64_t timeout_ns, bool stream_tiles, int32_t* ring, int32_t* ring_tail,
-                          bool early_gate, void* stream);
+                          int early_gate, void* stream);
 void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev, uint64_t timeout_ns, void* stream);
 int persistent_blocks_per_sm();
 void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,

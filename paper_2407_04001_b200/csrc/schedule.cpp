@@ -19,6 +19,7 @@
 // held or next to be claimed by its rank).
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <queue>
@@ -240,6 +241,45 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         }
     }
     const auto tt2 = std::chrono::steady_clock::now();
+    // ---- critical-path lead (PASE_LEAD_US): tasks of vertices with (almost) no slack in the
+    // simulated schedule move `lead` us earlier in the claim order, so a CTA holds them (waiting at
+    // the gate, warming its tile) BEFORE their children finish -- the duration model is coarse,
+    // and a chain task claimed after its children end costs the whole search that delay.  The
+    // order stays topological: a task never precedes a task of its vertex's children.
+    static const double kLead = std::getenv("PASE_LEAD_US") ? std::atof(std::getenv("PASE_LEAD_US")) : 0.0;
+    std::vector<double> key;
+    if (simulate && kLead > 0.0) {
+        std::vector<double> vs(n, 1e300), vf(n, 0.0);
+        for (int64_t t = 0; t < ntk; ++t)
+            if (all[t].vtx < n) {
+                vs[all[t].vtx] = std::min(vs[all[t].vtx], start[t]);
+                vf[all[t].vtx] = std::max(vf[all[t].vtx], start[t] + tdur[t]);
+            }
+        double span = 0.0;
+        for (int i = 0; i < n; ++i) span = std::max(span, vf[i]);
+        std::vector<double> lf(n, span);                // latest finish without delaying the root
+        for (int i = n - 1; i >= 0; --i)
+            if (P.parent[i] >= 0) lf[i] = lf[P.parent[i]] - (vf[P.parent[i]] - vs[P.parent[i]]);
+        static const double kSlack = std::getenv("PASE_LEAD_SLACK_US") ? std::atof(std::getenv("PASE_LEAD_SLACK_US")) : 2.0;
+        key.assign(start.begin(), start.end());
+        std::vector<double> vkey(n, -1e300);
+        for (int i = 0; i < n; ++i) {                   // children (lower ranks) first
+            double lo = -1e300;
+            for (int j : P.children[i]) lo = std::max(lo, vkey[j]);
+            if (nv > n)                                 // its cost-table chunks keep their start
+                for (int q = 0; q < G; ++q)
+                    for (int32_t t : tasks_of(n + i, q)) lo = std::max(lo, start[t]);
+            const bool crit = lf[i] - vf[i] <= kSlack;
+            for (int q = 0; q < G; ++q)
+                for (int32_t t : tasks_of(i, q)) {
+                    double k = crit ? start[t] - kLead : start[t];
+                    if (k <= lo) k = std::nextafter(lo, 1e300);
+                    key[t] = k;
+                    vkey[i] = std::max(vkey[i], k);
+                }
+        }
+        std::stable_sort(start_seq.begin(), start_seq.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+    }
     // ---- this rank's tasks in simulated start order
     std::vector<int32_t> mine;
     mine.reserve((size_t)ntk);

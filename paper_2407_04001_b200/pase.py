@@ -20,7 +20,7 @@ PASE_MAX_DIMS = 8
 PASE_MAX_HALO = 4
 PASE_MAX_DEP = 12
 PASE_HANDLE_BYTES = 256
-TRACE_WORDS = 6
+TRACE_WORDS = 22
 PASE_CFG_EXACT_P, PASE_CFG_LE_P = 0, 1
 STATUS = {0: "PASE_OK", 1: "PASE_ERR_INVALID", 2: "PASE_ERR_RESOURCE", 3: "PASE_ERR_CUDA",
           4: "PASE_ERR_NCCL", 5: "PASE_ERR_STATE"}
@@ -421,14 +421,15 @@ class Context:
 
     def trace(self) -> np.ndarray:
         """PASE_TRACE=1 timeline of the last solve, one row per DP task (ns, %globaltimer):
-        (rank, smid, t_claim, t_start, t_computed, t_synced, t_end)."""
+        (rank, smid, t_claim, t_start, t_computed, t_synced, t_end, then per warp 0..7
+        t_gate_seen, t_gate_fenced (0: no gate))."""
         n = self._L.pase_get_trace(self._h, None, 0)
         if n <= 0:
-            return np.zeros((0, 7), np.int64)
+            return np.zeros((0, TRACE_WORDS + 1), np.int64)
         buf = np.zeros(TRACE_WORDS * n, np.int64)
         self._L.pase_get_trace(self._h, _ptr(buf, C.c_int64), n)
         r = buf.reshape(n, TRACE_WORDS)
-        out = np.zeros((n, 7), np.int64)
+        out = np.zeros((n, TRACE_WORDS + 1), np.int64)
         out[:, 0] = r[:, 0] & 0xffffffff
         out[:, 1] = r[:, 0] >> 32
         out[:, 2:] = r[:, 1:]
