@@ -41,15 +41,30 @@ def build(force: bool = False, verbose: bool = False, out: str = SO, defines=())
     if not force and out == SO and not _stale():
         return SO
     import concurrent.futures as cf
+    import hashlib
     import tempfile
     tmp = tempfile.mkdtemp(prefix="pase_build_")
     flags = [*NVCC_FLAGS, *[f"-D{d}" for d in defines]]
+    # object cache (git-ignored, under build/): a source is recompiled only when it, a shared
+    # header or the flags change -- kernels.cu alone takes minutes
+    cache = os.path.join(ROOT, "build", "objcache")
+    os.makedirs(cache, exist_ok=True)
+    hdr = b"".join(open(os.path.join(CSRC, h), "rb").read() for h in HEADERS)
+    hdr += open(os.path.join(ROOT, "include", "pase.h"), "rb").read()
 
     def compile_one(src):
-        obj = os.path.join(tmp, os.path.splitext(src)[0] + ".o")
         extra = ["--split-compile=0"] if src.endswith(".cu") else []
+        key = hashlib.sha256(open(os.path.join(CSRC, src), "rb").read() + hdr +
+                             " ".join([NVCC, *flags, *extra]).encode()).hexdigest()[:24]
+        cached = os.path.join(cache, f"{os.path.splitext(src)[0]}-{key}.o")
+        if os.path.exists(cached):
+            return src, cached, subprocess.CompletedProcess([], 0, "", "")
+        obj = os.path.join(tmp, os.path.splitext(src)[0] + ".o")
         r = subprocess.run([NVCC, *flags, *extra, "-c", os.path.join(CSRC, src), "-o", obj],
                            capture_output=True, text=True)
+        if r.returncode == 0:
+            os.replace(obj, cached)
+            obj = cached
         return src, obj, r
 
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
@@ -66,9 +81,8 @@ def build(force: bool = False, verbose: bool = False, out: str = SO, defines=())
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link of libpase.so failed")
     os.replace(out + ".tmp", out)
-    for _, o, _ in results:
-        os.remove(o)
-    os.rmdir(tmp)
+    import shutil
+    shutil.rmtree(tmp, ignore_errors=True)
     return out
 
 

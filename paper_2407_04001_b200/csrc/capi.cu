@@ -265,6 +265,8 @@ bool no_2d() {
 // its K/G serial iterations -- the latency on the chain -- shrink, and the idle CTAs take the
 // extra tasks.  Non-critical vertices keep the efficient narrow groups (widening every
 // few-task vertex was measured slower, profiles/r01_ab_scheduling.txt).
+// widening keeps at least this many values of C per lane (PASE_WIDEN_MINC)
+const int kWidenMinC = std::getenv("PASE_WIDEN_MINC") ? std::max(1, std::atoi(std::getenv("PASE_WIDEN_MINC"))) : 8;
 void widen_critical(pase_ctx* ctx) {
     static const bool widen = !(std::getenv("PASE_WIDEN") && std::getenv("PASE_WIDEN")[0] == '0');
     if (!widen) return;
@@ -298,7 +300,7 @@ void widen_critical(pase_ctx* ctx) {
         for (int i = 0; i < n; ++i) {
             VertexDesc& d = ctx->vd[i];
             if (top[i] + bot[i] - w[i] < 0.85 * cp || d.shape < 0 || d.shape >= pase::kShapeG1 || d.wlog != 0) continue;
-            while (d.glog < 5 && (16 << d.glog) <= d.K && tasks_of(d) < nb) {
+            while (d.glog < 5 && (kWidenMinC << (d.glog + 1)) <= d.K && tasks_of(d) < nb) {
                 ++d.glog;
                 d.shape = (d.shape & ~3) | (d.glog - 2);
                 changed = true;
@@ -401,15 +403,13 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
 // children are still running when it is claimed runs its first work item once without stores
 // before the gate, so its tile's code is in this SM's instruction caches when the gate opens.
 // Bit 2 (PASE_GATE_ELECT=1): one warp per CTA polls the counter, the others a shared flag.
-// Bit 3 (PASE_CLAIM_AHEAD=1): a CTA claims its next task before releasing the current one.
 int early_gate() {
     static const int mode = [] {
         const char* e = std::getenv("PASE_EARLY_GATE");
         if (e && e[0] == '0') return 0;
         const char* w = std::getenv("PASE_WARM");
         const char* el = std::getenv("PASE_GATE_ELECT");
-        const char* ca = std::getenv("PASE_CLAIM_AHEAD");
-        return ((w && w[0] == '0') ? 1 : 3) | ((el && el[0] == '1') ? 4 : 0) | ((ca && ca[0] == '1') ? 8 : 0);
+        return ((w && w[0] == '0') ? 1 : 3) | ((el && el[0] == '1') ? 4 : 0);
     }();
     return mode;
 }
@@ -688,7 +688,14 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     // task; reset with the rest of the block
     const size_t pend_words = ((size_t)n + pase::kSchedLine - 1) / pase::kSchedLine * pase::kSchedLine;
     const size_t ring_off = pase::kSchedLine + pend_words + pase::kSchedLine;
-    const size_t sched_words = ctx->queue ? ring_off + std::max<size_t>(ctx->sp.tasks.size(), 1) : pase::kSchedLine + (size_t)n;
+    size_t sched_words = ctx->queue ? ring_off + std::max<size_t>(ctx->sp.tasks.size(), 1) : pase::kSchedLine + (size_t)n;
+    // dynamic vertices: one chunk counter per vertex on its own line, zeroed with the block
+    sched_words = (sched_words + pase::kSchedLine - 1) / pase::kSchedLine * pase::kSchedLine;
+    for (int i = 0; i < n; ++i)
+        if (ctx->sp.dyn[i]) {
+            ctx->vd[i].dctr = (int32_t)sched_words;
+            sched_words += pase::kSchedLine;
+        }
     ctx->sched_bytes = sizeof(int32_t) * sched_words;
     std::vector<Item> items2 = {                          // uploaded items first, as pool 1
         {(void**)&ctx->d_sched_init, ctx->sched_bytes},
@@ -1123,7 +1130,9 @@ pase_status pase_finish(pase_ctx* ctx, int32_t* configs_out, int32_t* config_ind
     ctx->launched = false;
     NvtxRange r("pase_finish (wait + strategy)");
     CUDA_TRY(cudaSetDevice(ctx->dev));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    // wait for THIS solve only (its end event): work queued behind it on the same stream -- e.g.
+    // the next search of a pipelined caller -- keeps running
+    CUDA_TRY(cudaEventSynchronize(ctx->ev1));
     if (ctx->stage_block) {                     // the create-time upload has completed
         stage_put(ctx->stage_block);
         ctx->stage_block = nullptr;
@@ -1272,9 +1281,10 @@ int64_t pase_get_schedule(const pase_ctx* ctx, int32_t* vinfo, int64_t* tasks, i
         }
     if (tasks)
         for (size_t t = 0; t < ctx->sp.tasks.size(); ++t) {
-            tasks[3 * t + 0] = ctx->sp.tasks[t].vtx;
-            tasks[3 * t + 1] = ctx->sp.tasks[t].i0;
-            tasks[3 * t + 2] = ctx->sp.tasks[t].i1;
+            tasks[4 * t + 0] = ctx->sp.tasks[t].vtx;
+            tasks[4 * t + 1] = ctx->sp.tasks[t].i0;
+            tasks[4 * t + 2] = ctx->sp.tasks[t].i1;
+            tasks[4 * t + 3] = ctx->sp.tasks[t].glog;
         }
     if (order) std::copy(ctx->sp.order.begin(), ctx->sp.order.end(), order);
     return (int64_t)ctx->sp.tasks.size();

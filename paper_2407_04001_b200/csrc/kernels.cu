@@ -10,6 +10,7 @@
 // ties in the min over C keep the lowest C (strict <, Fig. 5 line 17).
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 #include <type_traits>
 
@@ -1394,14 +1395,6 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
     __shared__ int s_task;
     __shared__ int s_warm;                                  // Gate::warm of the current task
     __shared__ int s_elect[2];                              // Gate::elect of the current task
-    // claim-ahead (early_gate bit 3): thread 0 claims the NEXT task as soon as its own warp has
-    // finished the current tile, so the claim's atomic and order lookup overlap the other warps'
-    // tails, the CTA barrier and the release.  Deadlock-free like the plain claim: a CTA's
-    // pending next task is later in the (topological) order than its unfinished current one.
-    __shared__ int s_next;
-    const bool ahead = !queue && (early_gate & 8);
-    int64_t t_claim_next = 0;
-    if (threadIdx.x == 0) s_next = -2;                      // -2: nothing claimed ahead
     __shared__ CostSmem csm;                                // cost-table tasks
     extern __shared__ __align__(128) unsigned char dyn[];   // stream-tile rings (launched with them
     const bool stream = stream_smem != 0;                   // only when a vertex uses a stream shape)
@@ -1414,11 +1407,7 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
     if (ld_relaxed(err) != 0) return;
     for (;;) {
         int64_t t_claim = 0, t_start = 0;
-        if (threadIdx.x == 0 && s_next != -2) {            // claimed ahead by the previous task
-            s_task = s_next;
-            s_next = -2;
-            t_claim = t_claim_next;
-        } else if (threadIdx.x == 0) {
+        if (threadIdx.x == 0) {
             if (trace) t_claim = (int64_t)globaltimer();
             const int s = atomicAdd(head, 1);
             if (!queue) {
@@ -1503,20 +1492,37 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
         if (task < 0) break;                                // timed out (reported via *err)
         // wave-tail tasks (schedule.cpp) run the vertex's tile with wider lane groups: every
         // tile family encodes log2(G) - 2 in the shape's low 2 bits
-        const int shape = tk.glog ? ((vd.shape & ~3) | (tk.glog - 2)) : vd.shape;
+        const int shape = tk.glog > 0 ? ((vd.shape & ~3) | (tk.glog - 2)) : vd.shape;
         const Gate gate{(early_gate && !queue) ? pending + tk.vtx : nullptr, err, timeout_ns, multi ? 1 : 0,
                         (early_gate & 4) ? s_elect : nullptr,
                         trace ? trace + (int64_t)kTraceWords * task + kTraceTaskWords : nullptr,
                         (early_gate && !queue) ? s_warm : 0};
         if (gate.stamp && (threadIdx.x & 31) == 0) gate.stamp[2 * warp] = gate.stamp[2 * warp + 1] = 0;
-        run_shape(shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1, red_b, red_c, dyn, seq, gate);
+        if (tk.glog >= 0) {
+            run_shape(shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1, red_b, red_c, dyn, seq, gate);
+        } else {
+            // slot of a dynamic vertex: each warp pulls warp rounds (-glog items) of [i0, i1) from
+            // the vertex's counter, the next one fetched while the current one runs; at most
+            // dquota rounds per warp (the host sizes slots x 8 x dquota >= rounds)
+            const int lane = threadIdx.x & 31;
+            const int32_t wch = -tk.glog;
+            int32_t* ctr = sched + vd.dctr;
+            Gate g = gate;
+            int c = 0;
+            if (lane == 0) c = atomicAdd(ctr, wch);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            for (int k = 0; k < vd.dquota; ++k) {
+                const int64_t c0 = tk.i0 + c;
+                if (c0 >= tk.i1) break;
+                int nxt = INT_MAX;
+                if (lane == 0 && k + 1 < vd.dquota) nxt = atomicAdd(ctr, wch);
+                run_shape(shape, vd, td, tds, 0, 1, c0, c0 + wch < tk.i1 ? c0 + wch : tk.i1, red_b, red_c, dyn, seq, g);
+                g.p = nullptr;                              // one gate per slot
+                c = __shfl_sync(0xffffffffu, nxt, 0);
+            }
+        }
         int64_t t_comp = 0, t_sync = 0;
         if (trace && threadIdx.x == 0) t_comp = (int64_t)globaltimer();
-        if (ahead && threadIdx.x == 0) {
-            if (trace) t_claim_next = (int64_t)globaltimer();
-            const int s = atomicAdd(head, 1);
-            s_next = s < ntasks ? order[s] : -1;
-        }
         __syncthreads();                                    // task's stores precede the release
         if (queue) {
             if (threadIdx.x == 0) {

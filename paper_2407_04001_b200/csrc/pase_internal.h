@@ -132,6 +132,10 @@ struct VertexDesc {          // one DP vertex (rank i)
     int32_t bcast;           // bit 0: write T to every rank, bit 1: write A to every rank
     int32_t pf_ahead;        // stream L2-prefetch form: items of lookahead (0 = the current item)
     int32_t npeer;           // peers written when bcast != 0 (world - 1)
+    // dynamic vertex: its tasks are "slots" that pull chunks of items from a
+    // per-solve counter in the scheduler block (sched[dctr], 0 = static tasks), at most dquota
+    // chunks per slot (nslots * dquota >= chunks, so every item is taken)
+    int32_t dctr, dquota;
     double* Tpeer[kMaxWorld - 1];     // this vertex's T / A in the peers' pools
     uint16_t* Apeer[kMaxWorld - 1];
 };
@@ -140,7 +144,9 @@ constexpr int kMaxTermsSh = 8;   // terms staged in shared memory (tiled shapes 
 
 struct TaskDesc {            // persistent schedule: item range [i0, i1) of vertex vtx
     int32_t vtx;
-    int32_t glog;            // 0: the vertex's lane groups; else log2 lanes per item (wave tail)
+    int32_t glog;            // 0: the vertex's lane groups; > 0: log2 lanes per item (wave tail);
+                             // < 0: a slot of a dynamic vertex pulling chunks of -glog items of
+                             // [i0, i1) (the rank's item range) from sched[dctr]
     int64_t i0, i1;
 };
 
@@ -159,6 +165,7 @@ struct SchedPlan {           // build_schedule output for one rank
     std::vector<int32_t> order;    // claim order (indices into tasks)
     std::vector<int32_t> pending;  // initial pending counter per vertex
     std::vector<int32_t> ready0;   // ready-queue mode: tasks ready at the start (no children), in order
+    std::vector<char> dyn;         // per vertex: run as dynamic slots (VertexDesc.dctr set by the caller)
     int64_t total_tasks = 0;       // over all ranks
 };
 

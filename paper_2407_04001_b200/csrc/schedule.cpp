@@ -29,6 +29,13 @@
 namespace pase {
 
 static const bool kWaveTail = !(std::getenv("PASE_WAVE_TAIL") && std::getenv("PASE_WAVE_TAIL")[0] == '0');
+// the wave tail's widened lane groups keep at least this many values of C per lane
+static const int kTailMinC = std::getenv("PASE_TAIL_MINC") ? std::max(1, std::atoi(std::getenv("PASE_TAIL_MINC"))) : 8;
+// dynamic vertices: a tiled vertex with at least kDynMin * nblocks static tasks
+// runs as <= nblocks slot tasks that pull one CTA round of items at a time from a counter --
+// no wave quantisation (a vertex of 1.15 waves of static tasks took 2 task durations)
+static const bool kDyn = std::getenv("PASE_DYN") && std::getenv("PASE_DYN")[0] == '1';
+static const double kDynMin = std::getenv("PASE_DYN_MIN") ? std::atof(std::getenv("PASE_DYN_MIN")) : 0.5;
 
 pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world, int rank, int nblocks,
                            SchedPlan& out, std::string& err, const std::vector<int32_t>* chunk_consumer,
@@ -44,7 +51,11 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     std::vector<GTask> all;
     {
         int64_t est = 0;                                // reserve: ~ items / spread tasks per vertex
-        for (int i = 0; i < n; ++i) est += std::min<int64_t>(spread, 1 + (vd[i].shape >= 0 ? vd[i].nitems : vd[i].nout) / 64);
+        for (int i = 0; i < n; ++i) {
+            const int64_t units = vd[i].shape >= 0 ? vd[i].nitems : vd[i].nout;
+            const int64_t groups = std::max<int64_t>(1, (256 >> vd[i].glog) >> vd[i].wlog);
+            est += std::min<int64_t>(spread, (units + groups - 1) / groups) + 2;
+        }
         all.reserve((size_t)(est * G + 16));
     }
     // tasks_of[i] for DP vertex i; tasks_of[n + i] = the cost-table chunks vertex i reads (run by
@@ -63,10 +74,21 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         int32_t operator[](size_t k) const { return b[k]; }
     };
     auto tasks_of = [&](int v, int q) { return Span{tidx.data() + toff[(size_t)v * G + q], tidx.data() + toff[(size_t)v * G + q + 1]}; };
+    out.dyn.assign(n, 0);
+    std::vector<int32_t> nslot_of(n, 0);
     for (int i = 0; i < n; ++i) {
-        const VertexDesc& d = vd[i];
+        VertexDesc& d = vd[i];
         const int64_t units = d.shape >= 0 ? d.nitems : d.nout;
         const int64_t groups = (256 >> d.glog) >> d.wlog;   // items a CTA runs concurrently
+        d.dctr = 0;
+        d.dquota = 0;
+        {
+            const int64_t local = units / (d.part ? G : 1);
+            const int64_t ti = std::max<int64_t>(groups, (local + spread - 1) / spread);
+            const int64_t tstatic = (local + ti - 1) / ti;
+            out.dyn[i] = kDyn && d.shape >= 0 && d.shape < kShapeStream && d.wlog == 0 &&
+                         (double)tstatic >= kDynMin * nblocks;
+        }
         for (int q = 0; q < G; ++q) {
             std::vector<std::pair<int64_t, int64_t>> runs;
             if (!d.part) {
@@ -85,6 +107,18 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
             }
             int64_t local = 0;
             for (auto& r : runs) local += r.second - r.first;
+            if (out.dyn[i]) {                               // slots over the rank's one item range
+                // each WARP pulls one warp round (gpw items) at a time; a slot's 8 warps take at
+                // most dquota rounds each, and ns * 8 * dquota >= the rounds, so every item is taken
+                const int64_t gpw = groups / 8;
+                const int64_t nch = (local + groups - 1) / groups, nwr = (local + gpw - 1) / gpw;
+                const int64_t ns = std::max<int64_t>(1, std::min<int64_t>(nch, nblocks));
+                if (q == rank) d.dquota = (int32_t)(2 * ((nwr + 8 * ns - 1) / (8 * ns)));
+                if (q == rank || nslot_of[i] == 0) nslot_of[i] = (int32_t)ns;
+                for (auto& r : runs)
+                    for (int64_t k = 0; k < ns; ++k) all.push_back({q, i, r.first, r.second, (int32_t)-gpw});
+                continue;
+            }
             int64_t ti = std::max<int64_t>(groups, (local + spread - 1) / spread);
             ti = (ti + groups - 1) / groups * groups;
             // wave tail: a vertex of one-round tasks spanning more than one wave of
@@ -100,7 +134,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
                     const int64_t bulk = (T / nblocks) * nblocks * ti;
                     const int64_t tail = local - bulk;
                     int g2 = d.glog;
-                    while (g2 < 5 && (16 << g2) <= d.K && tail * (int64_t(2) << g2) <= (int64_t)nblocks * 256) ++g2;
+                    while (g2 < 5 && (kTailMinC << (g2 + 1)) <= d.K && tail * (int64_t(2) << g2) <= (int64_t)nblocks * 256) ++g2;
                     if (g2 > d.glog) { bulk_end = runs[0].first + bulk; tail_glog = g2; }
                 }
             }
@@ -118,6 +152,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
             for (int q = 0; q < G; ++q) {
                 all.push_back({q, n + (*chunk_consumer)[c], c, c + 1, 0});
             }
+    const auto ttA = std::chrono::steady_clock::now();
     for (const GTask& t : all) ++toff[(size_t)t.vtx * G + t.rank + 1];
     for (size_t k = 1; k < toff.size(); ++k) toff[k] += toff[k - 1];
     tidx.resize(all.size());
@@ -125,6 +160,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         std::vector<int32_t> fill(toff.begin(), toff.end() - 1);
         for (size_t t = 0; t < all.size(); ++t) tidx[fill[(size_t)all[t].vtx * G + all[t].rank]++] = (int32_t)t;
     }
+    const auto ttB = std::chrono::steady_clock::now();
     // ---- broadcast flags (bit 0: T, bit 1: A)
     for (int j = 0; j < n; ++j) {
         VertexDesc& d = vd[j];
@@ -157,6 +193,7 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         if (pend[rank][p] > INT32_MAX) { err = "internal: pending counter overflow"; return PASE_ERR_RESOURCE; }
         out.pending[p] = (int32_t)pend[rank][p];
     }
+    const auto ttC = std::chrono::steady_clock::now();
     // ---- global list schedule: per-rank pools of nblocks CTAs, critical path first.
     // Estimated task time: ~3 us dependent-latency overhead + candidates at ~3e9/s per CTA.
     const int64_t ntk = (int64_t)all.size();
@@ -164,8 +201,9 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     for (int64_t t = 0; t < ntk; ++t) {
         if (all[t].vtx >= n) { tdur[t] = 4.0; continue; }  // a cost-table chunk
         const VertexDesc& d = vd[all[t].vtx];
-        const double cand = (double)(all[t].i1 - all[t].i0) * d.K * (d.shape < 0 ? 1 : d.q2 >= 0 ? kTile1 * kTile2 : kTile);  // G1 items: kTile outputs too
-        const double lanes = all[t].glog ? (double)(1 << (all[t].glog - d.glog)) : 1.0;   // wave tail
+        double cand = (double)(all[t].i1 - all[t].i0) * d.K * (d.shape < 0 ? 1 : d.q2 >= 0 ? kTile1 * kTile2 : kTile);  // G1 items: kTile outputs too
+        if (all[t].glog < 0) cand /= (double)std::max(1, nslot_of[all[t].vtx]);      // a slot's share
+        const double lanes = all[t].glog > 0 ? (double)(1 << (all[t].glog - d.glog)) : 1.0;   // wave tail
         tdur[t] = 3.0 + cand / (3000.0 * lanes);
     }
     for (int i = n - 1; i >= 0; --i) {                 // parents have higher ranks
@@ -313,8 +351,12 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         if (out.tasks[t].vtx >= 0 && out.pending[out.tasks[t].vtx] == 0) out.ready0.push_back(t);
     out.total_tasks = ntk;
     if (const char* tv = std::getenv("PASE_TIMING"); tv && tv[0] == '1')
-        std::fprintf(stderr, "[pase] schedule: tasks+pending %.3f ms, list-schedule %.3f ms, order %.3f ms (%lld tasks)\n",
+        std::fprintf(stderr, "[pase] schedule: tasks+pending %.3f ms (build %.3f, sort %.3f, flags+pending %.3f, durations %.3f), list-schedule %.3f ms, order %.3f ms (%lld tasks)\n",
                      std::chrono::duration<double, std::milli>(tt1 - tt0).count(),
+                     std::chrono::duration<double, std::milli>(ttA - tt0).count(),
+                     std::chrono::duration<double, std::milli>(ttB - ttA).count(),
+                     std::chrono::duration<double, std::milli>(ttC - ttB).count(),
+                     std::chrono::duration<double, std::milli>(tt1 - ttC).count(),
                      std::chrono::duration<double, std::milli>(tt2 - tt1).count(),
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tt2).count(),
                      (long long)ntk);

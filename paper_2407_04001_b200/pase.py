@@ -357,10 +357,10 @@ class Context:
 
     def schedule(self) -> Dict[str, np.ndarray]:
         """pase_get_schedule: per-vertex (part, bcast, ntasks, pending, shape, glog, wlog, q2),
-        tasks, claim order."""
+        tasks (vertex, first item, end item, kind: < 0 = slot of a dynamic vertex), claim order."""
         nt = self._L.pase_get_schedule(self._h, None, None, None)
         vinfo = np.zeros((self.n, 8), np.int32)
-        tasks = np.zeros((max(nt, 1), 3), np.int64)
+        tasks = np.zeros((max(nt, 1), 4), np.int64)
         order = np.zeros(max(nt, 1), np.int32)
         self._L.pase_get_schedule(self._h, _ptr(vinfo, C.c_int32), _ptr(tasks, C.c_int64), _ptr(order, C.c_int32))
         return {"vinfo": vinfo, "tasks": tasks[:nt], "order": order[:nt]}

@@ -7,7 +7,7 @@ import numpy as np
 from paper_2407_04001_b200 import pase, zoo
 tr = np.load("gpurun_out/trace_transformer.npy")
 c = pase.Context(zoo.bench_graph("transformer")[0], 64, policy="exact_p", device=-1)
-s = c.schedule(); order = s["order"]; tasks = s["tasks"].reshape(-1, 3)
+s = c.schedule(); order = s["order"]; tasks = s["tasks"].reshape(-1, 4)
 sigma, deps, parent = c.order(); n = len(sigma)
 vt = tr[:, 0].astype(int)
 dur = (tr[:, 5] - tr[:, 3]) / 1e3      # start -> sync (compute) ... trace columns: vtx,smid,claim,start,comp,sync,end
