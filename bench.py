@@ -283,6 +283,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="transformer", choices=sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-threads", type=int, default=1,
+                    help="host threads creating the next searches in the pipelined e2e (0: main thread only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--flush-mb", type=int, default=256)
     ap.add_argument("--no-alt", action="store_true", help="skip the throughput-regime (LE_P) line")
@@ -446,29 +448,44 @@ def main():
     # -- for independent searches issued back to back through the split API: search k+1 is
     # planned and enqueued on the host (pase_create + pase_launch) while the GPU runs search k,
     # then search k is finished (its own end event, pase_finish) and destroyed
-    e2e_pipe_ms = None
+    # With --e2e-threads T > 0, T host threads run pase_create of the next searches concurrently
+    # (ctypes releases the GIL; the library's process-wide caches are locked), the main thread
+    # launches them in order -- a planner serving a stream of requests.  Only for workloads whose
+    # contexts are small (at most 2 + T contexts are alive at once).
+    e2e_pipe_ms, e2e_threads = None, 0
     if world == 1 and args.e2e_steps > 0:
+        import concurrent.futures as cf
         nsteps = max(args.e2e_steps, 2)
-        with make_ctx_host() as cw:                 # warm the host caches
-            cw.solve()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        prev = None
-        for i in range(nsteps):
-            with torch.cuda.stream(stream):
-                flush.fill_(1)
-            c2 = make_ctx_host()
-            c2.launch()
-            if prev is not None:
+        with make_ctx_host() as cw:
+            small = int(cw.stats()["table_entries"]) * 10 < (2 << 30)   # T + A bytes
+        e2e_threads = args.e2e_threads if small else 0
+
+        def pipeline(steps):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            prev = None
+            with cf.ThreadPoolExecutor(max(1, e2e_threads)) as ex:
+                futs = []
+                for i in range(steps):
+                    while e2e_threads and len(futs) < min(steps, i + 1 + e2e_threads):
+                        futs.append(ex.submit(make_ctx_host))
+                    c2 = futs[i].result() if e2e_threads else make_ctx_host()
+                    with torch.cuda.stream(stream):
+                        flush.fill_(1)
+                    c2.launch()
+                    if prev is not None:
+                        prev.finish()
+                        prev.close()
+                    prev = c2
                 prev.finish()
                 prev.close()
-            prev = c2
-        prev.finish()
-        prev.close()
-        e1.record(stream)
-        e1.synchronize()
-        e2e_pipe_ms = e0.elapsed_time(e1) / nsteps
+            e1.record(stream)
+            e1.synchronize()
+            return e0.elapsed_time(e1) / steps
+
+        pipeline(min(nsteps, 4))                    # warm: pinned staging blocks, pool growth, threads
+        e2e_pipe_ms = pipeline(nsteps)
     e2e_value = cand / (e2e_pipe_ms / 1e3) if e2e_pipe_ms else e2e_serial_value
 
     if rank != 0:
@@ -526,7 +543,9 @@ def main():
         "e2e": {"value": e2e_value, "unit": "entries/s", "h2d_bytes_per_step": int(st["h2d_bytes"]),
                 "d2h_bytes_per_step": int(st["d2h_bytes"]),
                 "ms_per_step": e2e_pipe_ms if e2e_pipe_ms else e2e_tot / max(len(e2e_ms), 1),
-                "mode": ("pipelined: search k+1 created and launched on the host while the GPU runs search k"
+                "mode": (f"pipelined: the next searches created on {e2e_threads} host thread(s) while the GPU runs search k"
+                         if e2e_pipe_ms and e2e_threads else
+                         "pipelined: search k+1 created and launched on the host while the GPU runs search k"
                          if e2e_pipe_ms else "serial"),
                 "serial": {"value": e2e_serial_value, "ms_per_step": e2e_tot / max(len(e2e_ms), 1),
                            "what": "one search at a time: create, solve, destroy, then the next"},

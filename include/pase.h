@@ -266,10 +266,9 @@ pase_status pase_connect(pase_ctx* ctx, const void* blobs /* world * PASE_HANDLE
  * {partitioned, broadcast flags, this rank's task count, initial pending counter, kernel
  * shape (-1 generic, 0..63 1-D tile, >= 64 2-D tile), log2 lanes per item group, log2 warps
  * per item (latency mode), second tiled coordinate (-1 none)}; tasks =
- * this rank's {rank i, first item, end item, kind} quadruples (kind 0: the items [first, end);
- * > 0: the same, lane groups widened to 2^kind lanes (wave tail); < 0: a slot of a dynamic vertex
- * -- the vertex's slots together take the items [first, end) in warp rounds of -kind items from a
- * shared counter); order = claim order.  Returns the task count (arrays may be NULL). */
+ * this rank's {rank i, first item, end item, kind} quadruples (kind 0: the items [first, end)
+ * with the vertex's lane groups; > 0: with lane groups widened to 2^kind lanes (wave tail));
+ * order = claim order.  Returns the task count (arrays may be NULL). */
 int64_t pase_get_schedule(const pase_ctx* ctx, int32_t* vinfo, int64_t* tasks, int32_t* order);
 
 #ifdef __cplusplus

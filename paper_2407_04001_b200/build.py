@@ -63,6 +63,10 @@ def build(force: bool = False, verbose: bool = False, out: str = SO, defines=())
         r = subprocess.run([NVCC, *flags, *extra, "-c", os.path.join(CSRC, src), "-o", obj],
                            capture_output=True, text=True)
         if r.returncode == 0:
+            stem = os.path.splitext(src)[0] + "-"
+            for f in os.listdir(cache):                 # keep one object per source
+                if f.startswith(stem) and f.endswith(".o"):
+                    os.remove(os.path.join(cache, f))
             os.replace(obj, cached)
             obj = cached
         return src, obj, r

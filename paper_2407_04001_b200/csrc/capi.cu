@@ -64,7 +64,7 @@ struct pase_ctx {
     TermDesc* d_td = nullptr;
     pase::BtDesc* d_bt = nullptr;
     int32_t* d_bt_off = nullptr;
-    int nbtlev = 0;
+    int nbtlev = 0;                         // back-substitution levels
     int32_t* d_choice = nullptr;
     double* d_total = nullptr;
     int32_t* d_err = nullptr;               // scheduler time-out flag (inside the output block)
@@ -688,14 +688,8 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     // task; reset with the rest of the block
     const size_t pend_words = ((size_t)n + pase::kSchedLine - 1) / pase::kSchedLine * pase::kSchedLine;
     const size_t ring_off = pase::kSchedLine + pend_words + pase::kSchedLine;
-    size_t sched_words = ctx->queue ? ring_off + std::max<size_t>(ctx->sp.tasks.size(), 1) : pase::kSchedLine + (size_t)n;
-    // dynamic vertices: one chunk counter per vertex on its own line, zeroed with the block
-    sched_words = (sched_words + pase::kSchedLine - 1) / pase::kSchedLine * pase::kSchedLine;
-    for (int i = 0; i < n; ++i)
-        if (ctx->sp.dyn[i]) {
-            ctx->vd[i].dctr = (int32_t)sched_words;
-            sched_words += pase::kSchedLine;
-        }
+    const size_t sched_words = ctx->queue ? ring_off + std::max<size_t>(ctx->sp.tasks.size(), 1) : pase::kSchedLine + (size_t)n;
+
     ctx->sched_bytes = sizeof(int32_t) * sched_words;
     std::vector<Item> items2 = {                          // uploaded items first, as pool 1
         {(void**)&ctx->d_sched_init, ctx->sched_bytes},
@@ -723,7 +717,8 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     ctx->peers.rank = ctx->rank;
     ctx->peers.pending[ctx->rank] = ctx->d_sched + pase::kSchedLine;
     ctx->peers.bar[ctx->rank] = ctx->d_bar;
-    // back-substitution levels: lev(root) = 0, lev(i) = 1 + max lev over D(i)
+    // back-substitution: levels lev(root) = 0, lev(i) = 1 + max lev over D(i);
+    // the vertices of one level are independent, records in level order
     std::vector<int> blev(n, 0);
     int nlev = 0;
     for (int i = n - 1; i >= 0; --i) {
@@ -743,12 +738,17 @@ pase_status prepare(pase_ctx* ctx, bool device) {
             b = pase::BtDesc{};
             b.A = ctx->vd[i].A;
             b.node = P.sigma[i];
-            b.m = (int32_t)P.dep[i].size();
             b.K = P.K[P.sigma[i]];
-            for (int a = 0; a < b.m; ++a) { b.dep[a] = P.dep[i][a]; b.radix[a] = P.K[P.dep[i][a]]; }
+            int64_t st = 1;
+            for (size_t a = 0; a < P.dep[i].size(); ++a) {
+                b.dep[a] = P.dep[i][a];
+                b.stride[a] = st;
+                st *= P.K[P.dep[i][a]];
+            }
         }
     }
-    ctx->nbtlev = nlev;
+    const int ngroups = nlev;
+    ctx->nbtlev = ngroups;
     // one host image per pool (the uploaded prefix), one copy each
     // one upload image per pool (the uploaded prefix of each), staged in PINNED host memory
     // (a recycled process-wide block) so both copies run asynchronously at full PCIe rate;
@@ -780,7 +780,7 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     stage(img1, ctx->pool, ctx->d_vd, ctx->vd.data(), sizeof(VertexDesc) * n);
     stage(img1, ctx->pool, ctx->d_td, ctx->td.data(), sizeof(TermDesc) * ctx->td.size());
     stage(img1, ctx->pool, ctx->d_bt, bt.data(), sizeof(pase::BtDesc) * n);
-    stage(img1, ctx->pool, ctx->d_bt_off, bt_off.data(), sizeof(int32_t) * (nlev + 1));
+    stage(img1, ctx->pool, ctx->d_bt_off, bt_off.data(), sizeof(int32_t) * bt_off.size());
     stage(img2, ctx->pool2, ctx->d_sched_init, sched.data(), ctx->sched_bytes);
     stage(img2, ctx->pool2, ctx->d_tasks, ctx->sp.tasks.data(), sizeof(pase::TaskDesc) * ctx->sp.tasks.size());
     stage(img2, ctx->pool2, ctx->d_order, ctx->sp.order.data(), sizeof(int32_t) * ctx->sp.order.size());

@@ -10,7 +10,6 @@
 // ties in the min over C keep the lowest C (strict <, Fig. 5 line 17).
 #include <cuda_runtime.h>
 
-#include <climits>
 #include <cstdint>
 #include <type_traits>
 
@@ -109,7 +108,9 @@ __device__ __forceinline__ void stage_struct(T* dst, const T* src) {
 // per-axis shard extents (and prod need) are precomputed in shared memory, so the inner
 // loop is a min / multiply per axis, and stores are coalesced along the column.  Runs as its
 // own kernel (per-vertex launch schedule) or as tasks of the persistent DP kernel.
-__device__ __noinline__ void cost_chunk(const CostArgs& A, int chunk, CostSmem& sm) {
+// (force-inlined into both callers: the compiler then knows `sm` is shared memory -- LDS, not
+// generic loads -- and keeps the loop invariants of A in registers / the constant bank)
+__device__ __forceinline__ void cost_chunk(const CostArgs& A, int chunk, CostSmem& sm) {
     const CostChunk ch = A.chunks[chunk];
     // chunk.node = the vertex, or the edge's src: both structs are staged in one round of loads
     stage_struct(&sm.su, A.nodes + ch.node);
@@ -155,27 +156,51 @@ __device__ __noinline__ void cost_chunk(const CostArgs& A, int chunk, CostSmem& 
         sm.rowprod[rr] = pr;
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const bool lis = e.later_is_src != 0;
+    const double r = A.r;
+    double* const W = A.W + e.woff;
     for (int c0 = 0; c0 < Ke; c0 += kCostCols) {
         const int nc = min(kCostCols, Ke - c0);
         __syncthreads();
         for (int cc = threadIdx.x; cc < nc; cc += blockDim.x) {
             uint64_t pr = 1;
             for (int a = 0; a < nax; ++a) {
-                const uint32_t x = e.later_is_src ? need(c0 + cc, a) : held(c0 + cc, a);
+                const uint32_t x = lis ? need(c0 + cc, a) : held(c0 + cc, a);
                 sm.colq[a][cc] = x;
                 pr *= x;
             }
             sm.colprod[cc] = pr;
         }
         __syncthreads();
-        for (int rr = warp; rr < ch.nrows; rr += nw) {
-            double* out = A.W + e.woff + (int64_t)(ch.row0 + rr) * Ke + c0;
-            for (int cc = lane; cc < nc; cc += 32) {
-                uint64_t ov = 1;
-                for (int a = 0; a < nax; ++a) ov *= (uint64_t)min(sm.rowq[a][rr], sm.colq[a][cc]);
-                const uint64_t nd = e.later_is_src ? sm.colprod[cc] : sm.rowprod[rr];
-                out[cc] = __dmul_rn(A.r, __ull2double_rn((unsigned long long)(elem2 * (nd - ov))));
+        // rows: one warp each, columns over its lanes (coalesced stores); the axis loop is
+        // specialised on the axis count (registers, no per-axis branch)
+        auto rows = [&](auto nax_c) {
+            constexpr int NAX = decltype(nax_c)::value;
+            for (int rr = warp; rr < ch.nrows; rr += nw) {
+                uint32_t rq[NAX > 0 ? NAX : 1];         // this row's extents: registers
+#pragma unroll
+                for (int a = 0; a < NAX; ++a) rq[a] = sm.rowq[a][rr];
+                const uint64_t rp = sm.rowprod[rr];
+                double* out = W + (int64_t)(ch.row0 + rr) * Ke + c0;
+                for (int cc = lane; cc < nc; cc += 32) {
+                    uint64_t ov = 1;
+#pragma unroll
+                    for (int a = 0; a < NAX; ++a) ov *= (uint64_t)min(rq[a], sm.colq[a][cc]);
+                    const uint64_t nd = lis ? sm.colprod[cc] : rp;
+                    out[cc] = __dmul_rn(r, __ull2double_rn((unsigned long long)(elem2 * (nd - ov))));
+                }
             }
+        };
+        switch (nax) {
+            case 0: rows(std::integral_constant<int, 0>{}); break;
+            case 1: rows(std::integral_constant<int, 1>{}); break;
+            case 2: rows(std::integral_constant<int, 2>{}); break;
+            case 3: rows(std::integral_constant<int, 3>{}); break;
+            case 4: rows(std::integral_constant<int, 4>{}); break;
+            case 5: rows(std::integral_constant<int, 5>{}); break;
+            case 6: rows(std::integral_constant<int, 6>{}); break;
+            case 7: rows(std::integral_constant<int, 7>{}); break;
+            default: rows(std::integral_constant<int, kMaxDims>{}); break;
         }
     }
     __syncthreads();                                        // sm reused by the caller's next chunk
@@ -214,7 +239,8 @@ __device__ __forceinline__ void combine(double& b, int& c, double ob, int oc) {
 }
 
 // Item -> (combination of the untiled coordinates, tile index).  Single GPU: combinations
-// fastest (the warps of a CTA share a tile: L1 reuse).  Multi-GPU partitioned vertex (vd.part):
+// fastest (the warps of a CTA share a tile: L1 reuse; tiles-fastest was measured slower,
+// profiles/r02_ab_warm.txt).  Multi-GPU partitioned vertex (vd.part):
 // [combinations below the partition coordinate] fastest, then the tile, then the partition
 // coordinate -- so each rank's share of the vertex is ONE contiguous item range.
 // x / d for x < 2^31 with the host's magic numbers (VertexDesc, fastdiv_magic)
@@ -1498,29 +1524,7 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
                         trace ? trace + (int64_t)kTraceWords * task + kTraceTaskWords : nullptr,
                         (early_gate && !queue) ? s_warm : 0};
         if (gate.stamp && (threadIdx.x & 31) == 0) gate.stamp[2 * warp] = gate.stamp[2 * warp + 1] = 0;
-        if (tk.glog >= 0) {
-            run_shape(shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1, red_b, red_c, dyn, seq, gate);
-        } else {
-            // slot of a dynamic vertex: each warp pulls warp rounds (-glog items) of [i0, i1) from
-            // the vertex's counter, the next one fetched while the current one runs; at most
-            // dquota rounds per warp (the host sizes slots x 8 x dquota >= rounds)
-            const int lane = threadIdx.x & 31;
-            const int32_t wch = -tk.glog;
-            int32_t* ctr = sched + vd.dctr;
-            Gate g = gate;
-            int c = 0;
-            if (lane == 0) c = atomicAdd(ctr, wch);
-            c = __shfl_sync(0xffffffffu, c, 0);
-            for (int k = 0; k < vd.dquota; ++k) {
-                const int64_t c0 = tk.i0 + c;
-                if (c0 >= tk.i1) break;
-                int nxt = INT_MAX;
-                if (lane == 0 && k + 1 < vd.dquota) nxt = atomicAdd(ctr, wch);
-                run_shape(shape, vd, td, tds, 0, 1, c0, c0 + wch < tk.i1 ? c0 + wch : tk.i1, red_b, red_c, dyn, seq, g);
-                g.p = nullptr;                              // one gate per slot
-                c = __shfl_sync(0xffffffffu, nxt, 0);
-            }
-        }
+        run_shape(shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1, red_b, red_c, dyn, seq, gate);
         int64_t t_comp = 0, t_sync = 0;
         if (trace && threadIdx.x == 0) t_comp = (int64_t)globaltimer();
         __syncthreads();                                    // task's stores precede the release
@@ -1622,45 +1626,53 @@ int persistent_blocks_per_sm() {
 // K3: back-substitution: phi*(sigma_i) = A(i)[index(phi*|D(i))].  D(i) holds
 // only ancestors of i in the elimination tree, so all vertices of one "back level"
 // (1 + max back level over D(i); the root is level 0) are independent: one CTA walks the
-// levels, a thread per vertex, choices in shared memory.
+// levels, a thread per vertex, choices in shared memory.  The records are staged once with
+// 16-byte loads all in flight; a vertex's index is a branch-free sum over its (padded)
+// dependent list, so each level costs one dependent A(i) load (L2) plus a barrier.
 // =====================================================================================
-template <bool SMEM>
 __global__ void __launch_bounds__(256)
 backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt_off_g, int nlev, int n,
                  const double* __restrict__ root_T, int32_t* __restrict__ choice, double* __restrict__ total,
-                 int32_t* __restrict__ err, char* __restrict__ host_out) {
+                 int32_t* __restrict__ err, char* __restrict__ host_out, int smem_records) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    // SMEM: records and level offsets staged once (coalesced), choices kept on chip; only the
-    // A(i) reads of the dependent chain go to memory (L2-resident: the DP has just written them)
-    BtDesc* sh_bt = reinterpret_cast<BtDesc*>(smem_raw);
-    int32_t* sh_choice = reinterpret_cast<int32_t*>(smem_raw + sizeof(BtDesc) * (size_t)n);
-    int32_t* sh_off = sh_choice + n;
-    const BtDesc* bt = SMEM ? sh_bt : bt_g;
-    int32_t* ch = SMEM ? sh_choice : choice;
-    const int32_t* bt_off = SMEM ? sh_off : bt_off_g;
-    if (SMEM) {
-        const int words = (int)(sizeof(BtDesc) / 4) * n;
-        const int32_t* src = reinterpret_cast<const int32_t*>(bt_g);
-        int32_t* dst = reinterpret_cast<int32_t*>(sh_bt);
-        for (int k = threadIdx.x; k < words; k += blockDim.x) dst[k] = src[k];
-        for (int k = threadIdx.x; k <= nlev; k += blockDim.x) sh_off[k] = bt_off_g[k];
-        __syncthreads();
+    // [choices: n int32][level offsets: nlev + 1][records (smem_records)]
+    int32_t* ch = reinterpret_cast<int32_t*>(smem_raw);
+    int32_t* off = ch + n;
+    BtDesc* sh_bt = reinterpret_cast<BtDesc*>(smem_raw + (((size_t)n + nlev + 1) * 4 + 15) / 16 * 16);
+    const BtDesc* bt = smem_records ? sh_bt : bt_g;
+    if (smem_records) {                                     // 16-B words, 4 loads in flight per thread
+        static_assert(sizeof(BtDesc) % 16 == 0, "record copy in 16-B words");
+        const int words = (int)(sizeof(BtDesc) / 16) * n;
+        const uint4* src = reinterpret_cast<const uint4*>(bt_g);
+        uint4* dst = reinterpret_cast<uint4*>(sh_bt);
+        for (int k0 = threadIdx.x; k0 < words; k0 += 4 * blockDim.x) {
+            uint4 w[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k0 + u * (int)blockDim.x < words) w[u] = src[k0 + u * blockDim.x];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k0 + u * (int)blockDim.x < words) dst[k0 + u * blockDim.x] = w[u];
+        }
     }
+    for (int k = threadIdx.x; k <= nlev; k += blockDim.x) off[k] = bt_off_g[k];
+    for (int v = threadIdx.x; v < n; v += blockDim.x) ch[v] = 0;   // padding entries read ch[0]
     // a DP that reported an error (scheduler time-out) left tables unfinished: no lookups
     __shared__ int s_bad;
     if (threadIdx.x == 0) s_bad = 0;
-    __syncthreads();
     const int failed = *err;
+    __syncthreads();
     for (int lev = 0; lev < (failed ? 0 : nlev); ++lev) {
-        for (int k = bt_off[lev] + threadIdx.x; k < bt_off[lev + 1]; k += blockDim.x) {
+        for (int k = off[lev] + threadIdx.x; k < off[lev + 1]; k += blockDim.x) {
             const BtDesc& d = bt[k];
-            int64_t idx = 0, stride = 1;
-            for (int a = 0; a < d.m; ++a) {
-                idx += (int64_t)ch[d.dep[a]] * stride;
-                stride *= d.radix[a];
+            int c = 0;                                      // K = 1: A(i) is not stored
+            if (d.K > 1) {
+                int64_t idx = 0;
+#pragma unroll
+                for (int a = 0; a < kMaxDep; ++a) idx += (int64_t)ch[d.dep[a]] * d.stride[a];
+                c = d.A[idx];
+                if (c >= d.K) { s_bad = 1; c = 0; }        // no finite candidate: report, stay in range
             }
-            int c = d.K > 1 ? d.A[idx] : 0;                // K = 1: A(i) is not stored
-            if (c >= d.K) { s_bad = 1; c = 0; }           // no finite candidate: report, stay in range
             ch[d.node] = c;
         }
         __syncthreads();
@@ -1672,7 +1684,7 @@ backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt
     int32_t* hc = host_out ? reinterpret_cast<int32_t*>(host_out + 16) : nullptr;
     for (int v = threadIdx.x; v < n; v += blockDim.x) {
         const int32_t c = failed ? 0 : ch[v];
-        if (SMEM) choice[v] = c;
+        choice[v] = c;
         if (hc) hc[v] = c;
     }
     if (threadIdx.x == 0) {
@@ -1688,13 +1700,21 @@ backtrack_kernel(const BtDesc* __restrict__ bt_g, const int32_t* __restrict__ bt
 void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,
                       const double* root_T, int32_t* choice_dev, double* total_dev, int32_t* err_dev,
                       void* host_out, void* stream) {
-    const size_t smem = (sizeof(BtDesc) + sizeof(int32_t)) * (size_t)n + sizeof(int32_t) * (size_t)(nlev + 1);
-    if (smem <= 48 * 1024)
-        backtrack_kernel<true><<<1, 256, smem, (cudaStream_t)stream>>>(bt_dev, bt_off_dev, nlev, n, root_T,
-                                                                      choice_dev, total_dev, err_dev, (char*)host_out);
-    else
-        backtrack_kernel<false><<<1, 256, 0, (cudaStream_t)stream>>>(bt_dev, bt_off_dev, nlev, n, root_T,
-                                                                    choice_dev, total_dev, err_dev, (char*)host_out);
+    const size_t head = (((size_t)n + nlev + 1) * 4 + 15) / 16 * 16;
+    const size_t with_rec = head + sizeof(BtDesc) * (size_t)n;
+    // opt-in dynamic shared memory: the device maximum minus the kernel's static shared memory
+    static int max_dyn = [] {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, backtrack_kernel);
+        v -= (int)fa.sharedSizeBytes;
+        cudaFuncSetAttribute(backtrack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+        return v;
+    }();
+    const bool rec = with_rec <= (size_t)max_dyn;
+    backtrack_kernel<<<1, 256, rec ? with_rec : head, (cudaStream_t)stream>>>(
+        bt_dev, bt_off_dev, nlev, n, root_T, choice_dev, total_dev, err_dev, (char*)host_out, rec ? 1 : 0);
 }
 
 }  // namespace pase

@@ -132,10 +132,6 @@ struct VertexDesc {          // one DP vertex (rank i)
     int32_t bcast;           // bit 0: write T to every rank, bit 1: write A to every rank
     int32_t pf_ahead;        // stream L2-prefetch form: items of lookahead (0 = the current item)
     int32_t npeer;           // peers written when bcast != 0 (world - 1)
-    // dynamic vertex: its tasks are "slots" that pull chunks of items from a
-    // per-solve counter in the scheduler block (sched[dctr], 0 = static tasks), at most dquota
-    // chunks per slot (nslots * dquota >= chunks, so every item is taken)
-    int32_t dctr, dquota;
     double* Tpeer[kMaxWorld - 1];     // this vertex's T / A in the peers' pools
     uint16_t* Apeer[kMaxWorld - 1];
 };
@@ -144,9 +140,7 @@ constexpr int kMaxTermsSh = 8;   // terms staged in shared memory (tiled shapes 
 
 struct TaskDesc {            // persistent schedule: item range [i0, i1) of vertex vtx
     int32_t vtx;
-    int32_t glog;            // 0: the vertex's lane groups; > 0: log2 lanes per item (wave tail);
-                             // < 0: a slot of a dynamic vertex pulling chunks of -glog items of
-                             // [i0, i1) (the rank's item range) from sched[dctr]
+    int32_t glog;            // 0: the vertex's lane groups; > 0: log2 lanes per item (wave tail)
     int64_t i0, i1;
 };
 
@@ -165,7 +159,6 @@ struct SchedPlan {           // build_schedule output for one rank
     std::vector<int32_t> order;    // claim order (indices into tasks)
     std::vector<int32_t> pending;  // initial pending counter per vertex
     std::vector<int32_t> ready0;   // ready-queue mode: tasks ready at the start (no children), in order
-    std::vector<char> dyn;         // per vertex: run as dynamic slots (VertexDesc.dctr set by the caller)
     int64_t total_tasks = 0;       // over all ranks
 };
 
@@ -225,13 +218,12 @@ struct CostSmem {            // its shared memory ([axis][config]: conflict-free
     EdgeDesc se;
 };
 
-struct BtDesc {               // back-substitution record of one rank, in back-level order
+struct BtDesc {               // back-substitution record of one rank (DESIGN §5.4), in back-level order
     const uint16_t* A;       // argmin table A(i)
     int32_t node;            // sigma_i
     int32_t K;               // |C(sigma_i)|: a stored argmin >= K means no finite candidate
-    int32_t m;               // |D(i)|
-    int32_t dep[kMaxDep];    // D(i) node ids, ascending rank
-    int32_t radix[kMaxDep];
+    int32_t dep[kMaxDep];    // D(i) node ids (padding: node 0) ...
+    int64_t stride[kMaxDep]; // ... and their A(i) index strides (padding: 0)
 };
 
 struct EvalEdge {             // Eq. 1 kernels (eval.cu): W_e element = W[off + c_row * kcol + c_col]
@@ -252,7 +244,7 @@ void launch_dp_persistent(const VertexDesc* vd_dev, const TermDesc* td_dev, cons
                           int early_gate, void* stream);
 void launch_rank_barrier(const Peers& peers, int32_t* bar_dev, int32_t* err_dev, uint64_t timeout_ns, void* stream);
 int persistent_blocks_per_sm();
-void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int nlev, int n,
+void launch_backtrack(const BtDesc* bt_dev, const int32_t* bt_off_dev, int ngroups, int n,
                       const double* root_T, int32_t* choice_dev, double* total_dev, int32_t* err_dev,
                       void* host_out, void* stream);
 

@@ -19,7 +19,6 @@
 // held or next to be claimed by its rank).
 #include <algorithm>
 #include <chrono>
-#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <queue>
@@ -31,11 +30,6 @@ namespace pase {
 static const bool kWaveTail = !(std::getenv("PASE_WAVE_TAIL") && std::getenv("PASE_WAVE_TAIL")[0] == '0');
 // the wave tail's widened lane groups keep at least this many values of C per lane
 static const int kTailMinC = std::getenv("PASE_TAIL_MINC") ? std::max(1, std::atoi(std::getenv("PASE_TAIL_MINC"))) : 8;
-// dynamic vertices: a tiled vertex with at least kDynMin * nblocks static tasks
-// runs as <= nblocks slot tasks that pull one CTA round of items at a time from a counter --
-// no wave quantisation (a vertex of 1.15 waves of static tasks took 2 task durations)
-static const bool kDyn = std::getenv("PASE_DYN") && std::getenv("PASE_DYN")[0] == '1';
-static const double kDynMin = std::getenv("PASE_DYN_MIN") ? std::atof(std::getenv("PASE_DYN_MIN")) : 0.5;
 
 pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world, int rank, int nblocks,
                            SchedPlan& out, std::string& err, const std::vector<int32_t>* chunk_consumer,
@@ -74,21 +68,10 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         int32_t operator[](size_t k) const { return b[k]; }
     };
     auto tasks_of = [&](int v, int q) { return Span{tidx.data() + toff[(size_t)v * G + q], tidx.data() + toff[(size_t)v * G + q + 1]}; };
-    out.dyn.assign(n, 0);
-    std::vector<int32_t> nslot_of(n, 0);
     for (int i = 0; i < n; ++i) {
-        VertexDesc& d = vd[i];
+        const VertexDesc& d = vd[i];
         const int64_t units = d.shape >= 0 ? d.nitems : d.nout;
         const int64_t groups = (256 >> d.glog) >> d.wlog;   // items a CTA runs concurrently
-        d.dctr = 0;
-        d.dquota = 0;
-        {
-            const int64_t local = units / (d.part ? G : 1);
-            const int64_t ti = std::max<int64_t>(groups, (local + spread - 1) / spread);
-            const int64_t tstatic = (local + ti - 1) / ti;
-            out.dyn[i] = kDyn && d.shape >= 0 && d.shape < kShapeStream && d.wlog == 0 &&
-                         (double)tstatic >= kDynMin * nblocks;
-        }
         for (int q = 0; q < G; ++q) {
             std::vector<std::pair<int64_t, int64_t>> runs;
             if (!d.part) {
@@ -107,18 +90,6 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
             }
             int64_t local = 0;
             for (auto& r : runs) local += r.second - r.first;
-            if (out.dyn[i]) {                               // slots over the rank's one item range
-                // each WARP pulls one warp round (gpw items) at a time; a slot's 8 warps take at
-                // most dquota rounds each, and ns * 8 * dquota >= the rounds, so every item is taken
-                const int64_t gpw = groups / 8;
-                const int64_t nch = (local + groups - 1) / groups, nwr = (local + gpw - 1) / gpw;
-                const int64_t ns = std::max<int64_t>(1, std::min<int64_t>(nch, nblocks));
-                if (q == rank) d.dquota = (int32_t)(2 * ((nwr + 8 * ns - 1) / (8 * ns)));
-                if (q == rank || nslot_of[i] == 0) nslot_of[i] = (int32_t)ns;
-                for (auto& r : runs)
-                    for (int64_t k = 0; k < ns; ++k) all.push_back({q, i, r.first, r.second, (int32_t)-gpw});
-                continue;
-            }
             int64_t ti = std::max<int64_t>(groups, (local + spread - 1) / spread);
             ti = (ti + groups - 1) / groups * groups;
             // wave tail: a vertex of one-round tasks spanning more than one wave of
@@ -202,7 +173,6 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         if (all[t].vtx >= n) { tdur[t] = 4.0; continue; }  // a cost-table chunk
         const VertexDesc& d = vd[all[t].vtx];
         double cand = (double)(all[t].i1 - all[t].i0) * d.K * (d.shape < 0 ? 1 : d.q2 >= 0 ? kTile1 * kTile2 : kTile);  // G1 items: kTile outputs too
-        if (all[t].glog < 0) cand /= (double)std::max(1, nslot_of[all[t].vtx]);      // a slot's share
         const double lanes = all[t].glog > 0 ? (double)(1 << (all[t].glog - d.glog)) : 1.0;   // wave tail
         tdur[t] = 3.0 + cand / (3000.0 * lanes);
     }
@@ -279,45 +249,6 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         }
     }
     const auto tt2 = std::chrono::steady_clock::now();
-    // ---- critical-path lead (PASE_LEAD_US): tasks of vertices with (almost) no slack in the
-    // simulated schedule move `lead` us earlier in the claim order, so a CTA holds them (waiting at
-    // the gate, warming its tile) BEFORE their children finish -- the duration model is coarse,
-    // and a chain task claimed after its children end costs the whole search that delay.  The
-    // order stays topological: a task never precedes a task of its vertex's children.
-    static const double kLead = std::getenv("PASE_LEAD_US") ? std::atof(std::getenv("PASE_LEAD_US")) : 0.0;
-    std::vector<double> key;
-    if (simulate && kLead > 0.0) {
-        std::vector<double> vs(n, 1e300), vf(n, 0.0);
-        for (int64_t t = 0; t < ntk; ++t)
-            if (all[t].vtx < n) {
-                vs[all[t].vtx] = std::min(vs[all[t].vtx], start[t]);
-                vf[all[t].vtx] = std::max(vf[all[t].vtx], start[t] + tdur[t]);
-            }
-        double span = 0.0;
-        for (int i = 0; i < n; ++i) span = std::max(span, vf[i]);
-        std::vector<double> lf(n, span);                // latest finish without delaying the root
-        for (int i = n - 1; i >= 0; --i)
-            if (P.parent[i] >= 0) lf[i] = lf[P.parent[i]] - (vf[P.parent[i]] - vs[P.parent[i]]);
-        static const double kSlack = std::getenv("PASE_LEAD_SLACK_US") ? std::atof(std::getenv("PASE_LEAD_SLACK_US")) : 2.0;
-        key.assign(start.begin(), start.end());
-        std::vector<double> vkey(n, -1e300);
-        for (int i = 0; i < n; ++i) {                   // children (lower ranks) first
-            double lo = -1e300;
-            for (int j : P.children[i]) lo = std::max(lo, vkey[j]);
-            if (nv > n)                                 // its cost-table chunks keep their start
-                for (int q = 0; q < G; ++q)
-                    for (int32_t t : tasks_of(n + i, q)) lo = std::max(lo, start[t]);
-            const bool crit = lf[i] - vf[i] <= kSlack;
-            for (int q = 0; q < G; ++q)
-                for (int32_t t : tasks_of(i, q)) {
-                    double k = crit ? start[t] - kLead : start[t];
-                    if (k <= lo) k = std::nextafter(lo, 1e300);
-                    key[t] = k;
-                    vkey[i] = std::max(vkey[i], k);
-                }
-        }
-        std::stable_sort(start_seq.begin(), start_seq.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
-    }
     // ---- this rank's tasks in simulated start order
     std::vector<int32_t> mine;
     mine.reserve((size_t)ntk);

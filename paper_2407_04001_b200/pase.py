@@ -357,7 +357,7 @@ class Context:
 
     def schedule(self) -> Dict[str, np.ndarray]:
         """pase_get_schedule: per-vertex (part, bcast, ntasks, pending, shape, glog, wlog, q2),
-        tasks (vertex, first item, end item, kind: < 0 = slot of a dynamic vertex), claim order."""
+        tasks (vertex, first item, end item, kind: > 0 = wave-tail lane groups 2^kind), claim order."""
         nt = self._L.pase_get_schedule(self._h, None, None, None)
         vinfo = np.zeros((self.n, 8), np.int32)
         tasks = np.zeros((max(nt, 1), 4), np.int64)
