@@ -484,7 +484,7 @@ def main():
             e1.synchronize()
             return e0.elapsed_time(e1) / steps
 
-        pipeline(min(nsteps, 4))                    # warm: pinned staging blocks, pool growth, threads
+        pipeline(nsteps)                            # warm: pinned staging blocks, pool growth, threads
         e2e_pipe_ms = pipeline(nsteps)
     e2e_value = cand / (e2e_pipe_ms / 1e3) if e2e_pipe_ms else e2e_serial_value
 

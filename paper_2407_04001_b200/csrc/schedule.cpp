@@ -176,12 +176,13 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         const double lanes = all[t].glog > 0 ? (double)(1 << (all[t].glog - d.glog)) : 1.0;   // wave tail
         tdur[t] = 3.0 + cand / (3000.0 * lanes);
     }
+    std::vector<double> vtime(n, 0.0);
     for (int i = n - 1; i >= 0; --i) {                 // parents have higher ranks
         double work = 0.0, longest = 0.0;
         for (int q = 0; q < G; ++q)
             for (int32_t t : tasks_of(i, q)) { work += tdur[t]; longest = std::max(longest, tdur[t]); }
-        const double vt = std::max(longest, work / ((double)nblocks * G));
-        bl[i] = vt + (P.parent[i] >= 0 ? bl[P.parent[i]] : 0.0);
+        vtime[i] = std::max(longest, work / ((double)nblocks * G));
+        bl[i] = vtime[i] + (P.parent[i] >= 0 ? bl[P.parent[i]] : 0.0);
     }
     for (int i = n; i < nv; ++i) bl[i] = 4.0 + bl[i - n];
     const auto tt1 = std::chrono::steady_clock::now();
