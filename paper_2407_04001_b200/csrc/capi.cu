@@ -86,7 +86,8 @@ struct pase_ctx {
     int64_t total_tasks = 0;
     uint64_t timeout_ns = 4000000000ull;    // scheduler / barrier wait limit (PASE_SPIN_TIMEOUT_MS)
     bool persistent = true;
-    bool stream_tiles = false;              // some vertex uses the TMA-staged stream tile
+    bool stream_tiles = false;              // some vertex uses the TMA-staged stream tile or the
+                                            // CTA tile (the kernel gets the dynamic shared memory)
     bool cost_tasks = false;                // persistent: cost tables as tasks of the DP kernel
     // multi-GPU
     pase::Peers peers{};
@@ -267,6 +268,11 @@ bool no_2d() {
 // few-task vertex was measured slower, profiles/r01_ab_scheduling.txt).
 // widening keeps at least this many values of C per lane (PASE_WIDEN_MINC)
 const int kWidenMinC = std::getenv("PASE_WIDEN_MINC") ? std::max(1, std::atoi(std::getenv("PASE_WIDEN_MINC"))) : 8;
+// ... and 2 for vertices with K <= 64 (PASE_SMALLK_MINC): their reductions are short, so the
+// latency of the serial C loop, not the butterfly, dominates a widened task; they are widened
+// only while their tasks still fit one wave (GNMT -16 %, others neutral: profiles/r02_ab_warm.txt)
+const int kSmallKMinC = std::getenv("PASE_SMALLK_MINC") ? std::max(1, std::atoi(std::getenv("PASE_SMALLK_MINC"))) : 2;
+int widen_minc(int K) { return K <= 64 ? kSmallKMinC : kWidenMinC; }
 void widen_critical(pase_ctx* ctx) {
     static const bool widen = !(std::getenv("PASE_WIDEN") && std::getenv("PASE_WIDEN")[0] == '0');
     if (!widen) return;
@@ -300,7 +306,13 @@ void widen_critical(pase_ctx* ctx) {
         for (int i = 0; i < n; ++i) {
             VertexDesc& d = ctx->vd[i];
             if (top[i] + bot[i] - w[i] < 0.85 * cp || d.shape < 0 || d.shape >= pase::kShapeG1 || d.wlog != 0) continue;
-            while (d.glog < 5 && (kWidenMinC << (d.glog + 1)) <= d.K && tasks_of(d) < nb) {
+            while (d.glog < 5 && (widen_minc(d.K) << (d.glog + 1)) <= d.K && tasks_of(d) < nb) {
+                // a short reduction (K <= 64) is widened only while its tasks still fit one wave
+                if (d.K <= 64) {
+                    VertexDesc w = d;
+                    ++w.glog;
+                    if (tasks_of(w) > nb) break;
+                }
                 ++d.glog;
                 d.shape = (d.shape & ~3) | (d.glog - 2);
                 changed = true;
@@ -374,6 +386,30 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
             if (!big) d.glog = 3;
             set_tile2(d, q2, f2);
             d.shape = pase::kShape2S + ((f2 - 1) * 4 + form) * 4 + (d.glog - 2);
+            // CTA-tiled min-plus (PASE_CTA=1, single GPU): 4 groups of 64 threads, a 4 x 4 block
+            // of outputs per thread: cb2 = q2 values (<= 64), cb1 = qstar values balanced over the
+            // blocks; staged rounds of 32 values of C must fit the kernel's dynamic shared memory
+            static const bool cta = std::getenv("PASE_CTA") && std::getenv("PASE_CTA")[0] == '1';
+            if (cta && big && ctx->world == 1 && !d.part) {
+                const int rq = d.rq, rq2 = d.rq2;
+                const int cb2 = std::min(64, (rq2 + 3) / 4 * 4), T2 = cb2 / 4;
+                const int T1 = std::min(16, 64 / T2);
+                const int nblk1 = (rq + 4 * T1 - 1) / (4 * T1);
+                const int cb1 = ((rq + nblk1 - 1) / nblk1 + 3) / 4 * 4;
+                // two staging buffers and the final combine area in the kernel's dynamic smem
+                const size_t need = std::max<size_t>(2 * sizeof(double) * (size_t)pase::kCtaG * pase::kCtaCC *
+                                                     ((pase::kMaxP0 + 2) + (cb2 + 1) + 2 * (cb1 + 1)),
+                                                     (size_t)pase::kCtaG * 16 * 64 * 12);
+                if (T1 >= 1 && need <= pase::kCtaSmemMax) {
+                    d.cb1 = cb1;
+                    d.cb2 = cb2;
+                    d.ntile2 = (rq2 + cb2 - 1) / cb2;
+                    d.ntile = nblk1 * d.ntile2;
+                    d.nitems = d.ncombo * d.ntile;
+                    d.glog = 8;                           // one item per CTA round
+                    d.shape = pase::kShapeCta + (f2 - 1) * 4 + form;
+                }
+            }
             return;
         }
     }
@@ -657,7 +693,8 @@ pase_status prepare(pase_ctx* ctx, bool device) {
     const auto p1 = clk::now();
     widen_critical(ctx);
     ctx->stream_tiles = false;
-    for (const VertexDesc& d : ctx->vd) ctx->stream_tiles = ctx->stream_tiles || pase::stream_smem_shape(d.shape);
+    for (const VertexDesc& d : ctx->vd)
+        ctx->stream_tiles = ctx->stream_tiles || pase::stream_smem_shape(d.shape) || pase::cta_shape(d.shape);
     for (VertexDesc& d : ctx->vd) {                       // partitioned item order (split_item)
         d.psub = (d.part && d.shape >= 0) ? (int32_t)(d.ncombo / d.radix[d.m - 1]) : 1;
         // magic numbers of the work-item decode (division by invariant integers)

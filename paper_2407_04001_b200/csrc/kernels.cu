@@ -943,6 +943,7 @@ constexpr int kStreamStages = 4;                         // chunks per warp ring
 constexpr int kStreamRow = 34;                           // doubles per staged row chunk: 32 + alignment
 constexpr int kStreamStage = kTile * kStreamRow;         // doubles per stage (kTile rows)
 constexpr int kStreamWarps = 8;                          // warps per CTA (256 threads)
+static_assert(kCtaSmemMax <= (size_t)kStreamWarps * kStreamStages * kStreamStage * 8, "CTA tile in the ring area");
 constexpr size_t kStreamSmemBytes = (size_t)kStreamWarps * kStreamStages * kStreamStage * 8 +
                                     (size_t)kStreamWarps * kStreamStages * 8;
 
@@ -1211,6 +1212,200 @@ __device__ __noinline__ void tile_stream_pf(const VertexDesc& vd, const TermDesc
     }
 }
 
+// CTA-tiled min-plus (shape kShapeCta): the single-suffix structure of tile2s
+//   cost(j1, j2) = ((((P0 sum + A[j2]) + B) + S1[j1]) + S2)       (FORM as tile2s; canonical order)
+// with one CTA item = one combination x a cb1 x cb2 block of (qstar, q2).  Rounds of kCtaG *
+// kCtaCC values of C are staged in shared memory by cp.async (LDGSTS: no registers, every copy in
+// flight), double-buffered: round r + 1 is copied while round r is reduced.  A pass per round
+// forms p1[c][j2] = (P0 sum + A[j2]) (+ B) in place; then the CTA's kCtaG groups of 64 threads
+// each reduce kCtaCC values of C, every thread a 4 x 4 block of outputs (8 shared loads per 16
+// candidates, no address arithmetic, no cross-lane traffic).  The groups' (min, first argmin)
+// pairs are combined lexicographically at the end -- the oracle's strict < over increasing C --
+// so T, A stay bit-identical.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// shared doubles of one staging buffer (the host checks two of them fit kCtaSmemMax)
+__host__ __device__ constexpr int cta_buffer_doubles(int cb1, int cb2) {
+    return kCtaG * kCtaCC * ((kMaxP0 + 2) + (cb2 + 1) + 2 * (cb1 + 1));
+}
+
+template <int NP0, int FORM>
+__device__ __noinline__ void cta_items(const VertexDesc& vd, const TermDesc* td, int64_t i0, int64_t stride,
+                                       int64_t i1, unsigned char* dyn, Gate gate) {
+    constexpr int NB = FORM == 1 ? 1 : 0, NS2 = FORM == 2 ? 1 : FORM == 3 ? 2 : 0;
+    constexpr int TA = NP0, TS = NP0 + 1 + NB;
+    constexpr int CR = kCtaG * kCtaCC;                   // values of C per round
+    constexpr int NQ = NP0 + NB + (NS2 == 1 ? 1 : 0);    // per-C rows: P0 terms, B, constant S2
+    const int cb1 = vd.cb1, cb2 = vd.cb2;
+    const int T2 = cb2 >> 2, T1 = cb1 >> 2;
+    const int ld2 = cb2 + 1, ld1 = cb1 + 1;              // odd row pitch (doubles)
+    // buffer layout: q[NQ][CR] | p1[CR][ld2] | s1[CR][ld1] | s2[CR][ld1]
+    const int bufd = cta_buffer_doubles(cb1, cb2);
+    double* const base0 = reinterpret_cast<double*>(dyn);
+    const int tid = threadIdx.x;
+    const int grp = tid >> 6, u = tid & 63;
+    const int t2 = u % T2, t1 = u / T2;
+    const bool act = t1 < T1;
+    const int q1 = vd.qstar, q2 = vd.q2;
+    const int64_t sb = td[TA].stride[q2], ss = td[TS].stride[q1];
+    const int64_t ss2 = NS2 == 2 ? td[TS + 1].stride[q1] : 0;
+    const int K = vd.K;
+    bool live = !(gate.warm && gate.p);
+    for (int64_t it = i0; it < i1;) {
+        const uint32_t combo = fdiv((uint32_t)it, vd.mul_tile, vd.sh_tile);
+        const uint32_t blk = (uint32_t)it - combo * (uint32_t)vd.ntile;
+        const uint32_t b1 = fdiv(blk, vd.mul_tile2, vd.sh_tile2);
+        const int x1 = (int)b1 * cb1, x2 = (int)(blk - b1 * (uint32_t)vd.ntile2) * cb2;
+        const int nb1 = min(cb1, vd.rq - x1), nb2 = min(cb2, vd.rq2 - x2);
+        const double* pq[NQ > 0 ? NQ : 1];               // per-C rows: P0 terms, then B, then S2c
+        const double* pb = td[TA].base + (int64_t)x2 * sb;
+        const double* ps = td[TS].base + (int64_t)x1 * ss;
+        const double* pt2 = NS2 == 2 ? td[TS + 1].base + (int64_t)x1 * ss2 : nullptr;
+#pragma unroll
+        for (int t = 0; t < NP0; ++t) pq[t] = td[t].base;
+        if (NB) pq[NP0] = td[TA + 1].base;
+        if (NS2 == 1) pq[NP0 + NB] = td[TS + 1].base;
+        int64_t obase = 0, ost = 1;
+        uint32_t rem = combo;
+        for (int c = 0; c < vd.m; ++c) {                    // mixed-radix decode (lowest fastest)
+            const uint32_t r = (uint32_t)vd.radix[c];
+            if (c != q1 && c != q2) {
+                const uint32_t qv = fdiv(rem, vd.rmul[c], vd.rsh[c]);
+                const uint32_t v = rem - qv * r;
+                rem = qv;
+                obase += (int64_t)v * ost;
+#pragma unroll
+                for (int t = 0; t < NP0; ++t) pq[t] += (int64_t)v * td[t].stride[c];
+                if (NB) pq[NP0] += (int64_t)v * td[TA + 1].stride[c];
+                if (NS2 == 1) pq[NP0 + NB] += (int64_t)v * td[TS + 1].stride[c];
+                pb += (int64_t)v * td[TA].stride[c];
+                ps += (int64_t)v * td[TS].stride[c];
+                if (NS2 == 2) pt2 += (int64_t)v * td[TS + 1].stride[c];
+            }
+            ost *= r;
+        }
+        double best[16];
+        int bestC[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) { best[j] = __longlong_as_double(0x7ff0000000000000ll); bestC[j] = 0x7fffffff; }
+        const int Kc = live ? K : min(K, CR);            // warm: one round
+        const int nr = (Kc + CR - 1) / CR;
+        // copy round r into buffer r & 1 (every thread issues its share; rows clamped to the block)
+        auto issue = [&](int r) {
+            double* B = base0 + (r & 1) * bufd;
+            double* qs = B;
+            double* as = qs + (kMaxP0 + 2) * CR;
+            double* s1 = as + CR * ld2;
+            double* s2 = s1 + CR * ld1;
+            const int c0 = r * CR, nc = min(CR, Kc - c0);
+            for (int x = tid; x < NQ * CR; x += blockDim.x) {
+                const int c = x % CR, t = x / CR;
+                if (c < nc) cp_async8(qs + t * CR + c, pq[t] + c0 + c);
+            }
+            for (int x = tid; x < CR * cb2; x += blockDim.x) {
+                const int c = x % CR, jj = x / CR;
+                if (c < nc) cp_async8(as + c * ld2 + jj, pb + (int64_t)min(jj, nb2 - 1) * sb + c0 + c);
+            }
+            for (int x = tid; x < CR * cb1; x += blockDim.x) {
+                const int c = x % CR, jj = x / CR;
+                if (c < nc) {
+                    cp_async8(s1 + c * ld1 + jj, ps + (int64_t)min(jj, nb1 - 1) * ss + c0 + c);
+                    if (NS2 == 2) cp_async8(s2 + c * ld1 + jj, pt2 + (int64_t)min(jj, nb1 - 1) * ss2 + c0 + c);
+                }
+            }
+            cp_async_commit();
+        };
+        if (live) gate_wait(gate);                          // (each warp; the barrier below joins them)
+        __syncthreads();                                    // the previous item's buffers are free
+        if (nr > 0) issue(0);
+        for (int r = 0; r < nr; ++r) {
+            if (r + 1 < nr) { issue(r + 1); cp_async_wait<1>(); } else { cp_async_wait<0>(); }
+            __syncthreads();                                // round r landed (every thread's copies)
+            double* B = base0 + (r & 1) * bufd;
+            double* qs = B;
+            double* as = qs + (kMaxP0 + 2) * CR;
+            double* s1 = as + CR * ld2;
+            double* s2 = s1 + CR * ld1;
+            const int c0 = r * CR, nc = min(CR, Kc - c0);
+            // p1[c][j2] = ((P0 sum) + A[j2]) (+ B), in place over the staged A
+            for (int x = tid; x < CR * cb2; x += blockDim.x) {
+                const int c = x % CR, jj = x / CR;
+                if (c < nc) {
+                    double pre = qs[c];
+#pragma unroll
+                    for (int t = 1; t < NP0; ++t) pre = __dadd_rn(pre, qs[t * CR + c]);
+                    double v = __dadd_rn(pre, as[c * ld2 + jj]);
+                    if (NB) v = __dadd_rn(v, qs[NP0 * CR + c]);
+                    as[c * ld2 + jj] = v;
+                }
+            }
+            __syncthreads();
+            const int ce = min(kCtaCC * (grp + 1), nc);
+            if (act) {
+#pragma unroll 2
+                for (int c = kCtaCC * grp; c < ce; ++c) {
+                    double p[4], sv[4], s2v[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        p[k] = as[c * ld2 + 4 * t2 + k];
+                        sv[k] = s1[c * ld1 + 4 * t1 + k];
+                        if (NS2 == 2) s2v[k] = s2[c * ld1 + 4 * t1 + k];
+                    }
+                    const double s2c = NS2 == 1 ? qs[(NP0 + NB) * CR + c] : 0.0;
+                    const int C = c0 + c;
+#pragma unroll
+                    for (int j1 = 0; j1 < 4; ++j1)
+#pragma unroll
+                        for (int j2 = 0; j2 < 4; ++j2) {
+                            double cost = __dadd_rn(p[j2], sv[j1]);
+                            if (NS2 == 1) cost = __dadd_rn(cost, s2c);
+                            if (NS2 == 2) cost = __dadd_rn(cost, s2v[j1]);
+                            const int j = j1 * 4 + j2;
+                            if (cost < best[j]) { best[j] = cost; bestC[j] = C; }   // strict <: lowest C
+                        }
+                }
+            }
+            __syncthreads();                                // buffer r & 1 is refilled by round r + 2
+        }
+        // combine the groups' partial (min, argmin) per output: [g][j][u] in the staging area
+        double* rb = base0;
+        int* rc = reinterpret_cast<int*>(rb + kCtaG * 16 * 64);
+        if (grp > 0) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                rb[(grp * 16 + j) * 64 + u] = best[j];
+                rc[(grp * 16 + j) * 64 + u] = bestC[j];
+            }
+        }
+        __syncthreads();
+        if (grp == 0 && act) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                for (int g2 = 1; g2 < kCtaG; ++g2)
+                    combine(best[j], bestC[j], rb[(g2 * 16 + j) * 64 + u], rc[(g2 * 16 + j) * 64 + u]);
+            if (live) {
+#pragma unroll
+                for (int j1 = 0; j1 < 4; ++j1)
+#pragma unroll
+                    for (int j2 = 0; j2 < 4; ++j2) {
+                        const int a1 = 4 * t1 + j1, a2 = 4 * t2 + j2;
+                        if (a1 < nb1 && a2 < nb2)
+                            st_out(vd, obase + (int64_t)(x1 + a1) * vd.ostride_q + (int64_t)(x2 + a2) * vd.ostride_q2,
+                                   best[j1 * 4 + j2], bestC[j1 * 4 + j2]);
+                    }
+            }
+        }
+        if (live) it += stride;
+        live = true;
+    }
+}
+
 // shape index: 0..63 = tiled (NP-1)*16 + NS*4 + (log2 G - 2); -1 = generic
 //   first_warp / nwarps: the calling warp's index / the warps sharing [i0, i1) (a CTA's warps
 //   are consecutive).  Item slots per warp: 32/G (throughput mode) or 1/W (latency mode).
@@ -1287,6 +1482,14 @@ __device__ __forceinline__ void run_shape(int shape, const VertexDesc& vd, const
 #undef PASE_2S_FORMS
 #undef PASE_2S_G
 #undef PASE_CASE2S
+#define PASE_CASEC(NP0, FORM)                                                                     \
+    case kShapeCta + (NP0 - 1) * 4 + FORM:                                                        \
+        cta_items<NP0, FORM>(vd, td_sh, i0 + (first_warp >> 3), nwarps >> 3, i1, dyn, gate);      \
+        return;
+        PASE_CASEC(1, 0) PASE_CASEC(1, 1) PASE_CASEC(1, 2) PASE_CASEC(1, 3)
+        PASE_CASEC(2, 0) PASE_CASEC(2, 1) PASE_CASEC(2, 2) PASE_CASEC(2, 3)
+        PASE_CASEC(3, 0) PASE_CASEC(3, 1) PASE_CASEC(3, 2) PASE_CASEC(3, 3)
+#undef PASE_CASEC
         default: {
             const int gpw = 32 >> vd.glog;
             generic_items(vd, tds_g, vd.glog, i0 + first_warp * gpw, nwarps * gpw, i1, gate);
@@ -1306,7 +1509,7 @@ dp_fill_vertex(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ 
     const int nt = min(vds[vtx].nterms, kMaxTermsSh);
     for (int t = threadIdx.x; t < nt; t += blockDim.x) td[t] = tds[vds[vtx].term0 + t];
     __syncthreads();
-    if (stream_smem_shape(vd.shape)) stream_init(dyn);
+    if (stream_smem_shape(vd.shape)) stream_init(dyn);      // (the CTA tile uses the ring area's head)
     uint32_t seq = 0;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1321,7 +1524,7 @@ void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vert
     const int64_t units = vh.shape >= 0 ? vh.nitems : vh.nout;
     int64_t blocks = ((units * G << vh.wlog) + threads - 1) / threads;
     blocks = blocks > 148 * 8 ? 148 * 8 : (blocks < 1 ? 1 : blocks);
-    const size_t dyn = stream_smem_shape(vh.shape) ? kStreamSmemBytes : 0;
+    const size_t dyn = (stream_smem_shape(vh.shape) || cta_shape(vh.shape)) ? kStreamSmemBytes : 0;
     if (dyn) {
         static bool attr = (cudaFuncSetAttribute(dp_fill_vertex, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)kStreamSmemBytes), true);

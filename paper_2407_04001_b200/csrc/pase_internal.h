@@ -131,6 +131,7 @@ struct VertexDesc {          // one DP vertex (rank i)
     int32_t psub;            // partitioned: combinations below the top coordinate (ncombo / K_top)
     int32_t bcast;           // bit 0: write T to every rank, bit 1: write A to every rank
     int32_t pf_ahead;        // stream L2-prefetch form: items of lookahead (0 = the current item)
+    int32_t cb1, cb2;        // CTA-tiled shape: block of (qstar, q2) values per CTA item (multiples of 4)
     int32_t npeer;           // peers written when bcast != 0 (world - 1)
     double* Tpeer[kMaxWorld - 1];     // this vertex's T / A in the peers' pools
     uint16_t* Apeer[kMaxWorld - 1];
@@ -181,6 +182,16 @@ constexpr int kShapeStreamPF = 224;     // [224, 256): 1-D tile, G = 32, next it
 __host__ __device__
 #endif
 constexpr bool stream_smem_shape(int s) { return s >= kShapeStream && s < kShapeStreamPF; }
+// [256, 268): CTA-tiled min-plus, the single-suffix structure of kShape2S:
+// (NP0 - 1) * 4 + form; one CTA item = one combination x a cb1 x cb2 block of (qstar, q2)
+constexpr int kShapeCta = 256;
+constexpr int kCtaCC = 8;               // values of C per thread group per staged round
+constexpr int kCtaG = 4;                // thread groups of 64 per CTA (each reduces its own C run)
+constexpr size_t kCtaSmemMax = 69632;   // dynamic shared memory the persistent kernel gets
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr bool cta_shape(int s) { return s >= kShapeCta && s < kShapeCta + 12; }
 //   form 0: P1 = [A], S = [S1]; 1: P1 = [A, B], S = [S1]; 2: S = [S1, const]; 3: S = [S1, S2 on q1]
 constexpr int kMaxP0 = 4, kMaxP1 = 2;   // 2-D tile: max scalar-prefix / q2-prefix terms
 #ifndef PASE_COST_ROWS

@@ -30,6 +30,7 @@ namespace pase {
 static const bool kWaveTail = !(std::getenv("PASE_WAVE_TAIL") && std::getenv("PASE_WAVE_TAIL")[0] == '0');
 // the wave tail's widened lane groups keep at least this many values of C per lane
 static const int kTailMinC = std::getenv("PASE_TAIL_MINC") ? std::max(1, std::atoi(std::getenv("PASE_TAIL_MINC"))) : 8;
+static const int kTailSmallKMinC = std::getenv("PASE_TAIL_SMALLK_MINC") ? std::max(1, std::atoi(std::getenv("PASE_TAIL_SMALLK_MINC"))) : kTailMinC;
 
 pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world, int rank, int nblocks,
                            SchedPlan& out, std::string& err, const std::vector<int32_t>* chunk_consumer,
@@ -105,7 +106,8 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
                     const int64_t bulk = (T / nblocks) * nblocks * ti;
                     const int64_t tail = local - bulk;
                     int g2 = d.glog;
-                    while (g2 < 5 && (kTailMinC << (g2 + 1)) <= d.K && tail * (int64_t(2) << g2) <= (int64_t)nblocks * 256) ++g2;
+                    const int minc = d.K <= 64 ? kTailSmallKMinC : kTailMinC;
+                    while (g2 < 5 && (minc << (g2 + 1)) <= d.K && tail * (int64_t(2) << g2) <= (int64_t)nblocks * 256) ++g2;
                     if (g2 > d.glog) { bulk_end = runs[0].first + bulk; tail_glog = g2; }
                 }
             }
@@ -172,7 +174,8 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     for (int64_t t = 0; t < ntk; ++t) {
         if (all[t].vtx >= n) { tdur[t] = 4.0; continue; }  // a cost-table chunk
         const VertexDesc& d = vd[all[t].vtx];
-        double cand = (double)(all[t].i1 - all[t].i0) * d.K * (d.shape < 0 ? 1 : d.q2 >= 0 ? kTile1 * kTile2 : kTile);  // G1 items: kTile outputs too
+        const double outs = d.shape < 0 ? 1 : cta_shape(d.shape) ? (double)d.cb1 * d.cb2 : d.q2 >= 0 ? kTile1 * kTile2 : kTile;
+        double cand = (double)(all[t].i1 - all[t].i0) * d.K * outs;   // G1 items: kTile outputs too
         const double lanes = all[t].glog > 0 ? (double)(1 << (all[t].glog - d.glog)) : 1.0;   // wave tail
         tdur[t] = 3.0 + cand / (3000.0 * lanes);
     }
