@@ -278,6 +278,20 @@ void widen_critical(pase_ctx* ctx) {
     if (!widen) return;
     const Plan& P = ctx->P;
     const int n = P.n;
+    // task-length cap (A/B, PASE_MAX_LANE_CAND): a one-round task of a big vertex occupies its CTA
+    // for outputs-per-item x K/G serial candidates per lane; while that exceeds the cap, widen
+    // the lane groups (shorter, more numerous tasks: a ready critical task waits less for a CTA)
+    static const int64_t cap = std::getenv("PASE_MAX_LANE_CAND") ? std::atoll(std::getenv("PASE_MAX_LANE_CAND")) : 0;
+    if (cap > 0)
+        for (VertexDesc& d : ctx->vd) {
+            if (d.shape < 0 || d.shape >= pase::kShapeG1 || d.wlog != 0) continue;
+            const int64_t outs = d.q2 >= 0 ? pase::kTile1 * pase::kTile2 : pase::kTile;
+            while (d.glog < 5 && (widen_minc(d.K) << (d.glog + 1)) <= d.K &&
+                   outs * ((d.K + (1 << d.glog) - 1) >> d.glog) > cap) {
+                ++d.glog;
+                d.shape = (d.shape & ~3) | (d.glog - 2);
+            }
+        }
     const int64_t nb = ctx->nblocks;
     auto tasks_of = [&](const VertexDesc& d) -> int64_t {
         const int64_t items = std::max<int64_t>(1, d.nitems / (d.part ? ctx->world : 1));

@@ -27,6 +27,9 @@ constexpr int kCUnroll = PASE_CUNROLL;
 #ifndef PASE_ACQ_FENCE
 #define PASE_ACQ_FENCE 1       // acquire via fence.acq_rel after the relaxed poll (else ld.acquire)
 #endif
+#ifndef PASE_GATE_LDACQ
+#define PASE_GATE_LDACQ 0      // per-warp gate: acquire via ld.acquire of the counter instead of a fence
+#endif
 #ifndef PASE_REL_RED
 #define PASE_REL_RED 0         // release via red.release (no return) instead of atom.acq_rel
 #endif
@@ -361,6 +364,7 @@ __device__ __forceinline__ void gate_wait(Gate& g) {
         }
         if (g.stamp) g.stamp[2 * (threadIdx.x >> 5)] = (int64_t)gate_clock();
         if (g.multi) { int v; asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(g.p) : "memory"); (void)v; }
+        else if (PASE_GATE_LDACQ) { int v; asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(g.p) : "memory"); (void)v; }
         else asm volatile("fence.acq_rel.gpu;" ::: "memory");
         if (poller && g.elect) st_shared_relaxed(g.elect + 1, 1);
         if (g.stamp) g.stamp[2 * (threadIdx.x >> 5) + 1] = (int64_t)gate_clock();

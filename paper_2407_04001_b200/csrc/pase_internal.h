@@ -192,6 +192,11 @@ constexpr size_t kCtaSmemMax = 69632;   // dynamic shared memory the persistent 
 __host__ __device__
 #endif
 constexpr bool cta_shape(int s) { return s >= kShapeCta && s < kShapeCta + 12; }
+// list-schedule task-duration families (schedule.cpp dur_model)
+enum { kDurGeneric, kDurLatency, kDur1D, kDur2D, kDur2S, kDurG1, kDurStream, kDurCta, kDurFamilies };
+struct DurModel { double a[kDurFamilies], rate[kDurFamilies]; };
+int dur_family(const VertexDesc& d);
+const DurModel& dur_model();
 //   form 0: P1 = [A], S = [S1]; 1: P1 = [A, B], S = [S1]; 2: S = [S1, const]; 3: S = [S1, S2 on q1]
 constexpr int kMaxP0 = 4, kMaxP1 = 2;   // 2-D tile: max scalar-prefix / q2-prefix terms
 #ifndef PASE_COST_ROWS

@@ -21,6 +21,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <queue>
 
 #include "pase_internal.h"
@@ -31,6 +32,39 @@ static const bool kWaveTail = !(std::getenv("PASE_WAVE_TAIL") && std::getenv("PA
 // the wave tail's widened lane groups keep at least this many values of C per lane
 static const int kTailMinC = std::getenv("PASE_TAIL_MINC") ? std::max(1, std::atoi(std::getenv("PASE_TAIL_MINC"))) : 8;
 static const int kTailSmallKMinC = std::getenv("PASE_TAIL_SMALLK_MINC") ? std::max(1, std::atoi(std::getenv("PASE_TAIL_SMALLK_MINC"))) : kTailMinC;
+
+// Task-duration model of the list schedule: a fixed latency plus candidates at a per-tile-family
+// rate (us, candidates per us per CTA).  PASE_DUR="f:a:rate,..." overrides family f (A/B only).
+int dur_family(const VertexDesc& d) {
+    if (d.shape < 0) return kDurGeneric;
+    if (d.wlog > 0) return kDurLatency;
+    if (d.shape < kShape2D) return kDur1D;
+    if (d.shape < kShape2S) return kDur2D;
+    if (d.shape < kShapeG1) return kDur2S;
+    if (d.shape < kShapeStream) return kDurG1;
+    if (d.shape < kShapeCta) return kDurStream;
+    return kDurCta;
+}
+const DurModel& dur_model() {
+    static const DurModel m = [] {
+        DurModel r;
+        for (int f = 0; f < kDurFamilies; ++f) { r.a[f] = 3.0; r.rate[f] = 3000.0; }
+        if (const char* e = std::getenv("PASE_DUR")) {
+            int f;
+            double a, rate;
+            for (const char* q = e; q && *q;) {
+                if (std::sscanf(q, "%d:%lf:%lf", &f, &a, &rate) == 3 && f >= 0 && f < kDurFamilies && rate > 0) {
+                    r.a[f] = a;
+                    r.rate[f] = rate;
+                }
+                q = std::strchr(q, ',');
+                if (q) ++q;
+            }
+        }
+        return r;
+    }();
+    return m;
+}
 
 pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world, int rank, int nblocks,
                            SchedPlan& out, std::string& err, const std::vector<int32_t>* chunk_consumer,
@@ -171,13 +205,15 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     // Estimated task time: ~3 us dependent-latency overhead + candidates at ~3e9/s per CTA.
     const int64_t ntk = (int64_t)all.size();
     std::vector<double> tdur(ntk), bl(nv, 0.0);
+    const DurModel& dm = dur_model();
     for (int64_t t = 0; t < ntk; ++t) {
         if (all[t].vtx >= n) { tdur[t] = 4.0; continue; }  // a cost-table chunk
         const VertexDesc& d = vd[all[t].vtx];
         const double outs = d.shape < 0 ? 1 : cta_shape(d.shape) ? (double)d.cb1 * d.cb2 : d.q2 >= 0 ? kTile1 * kTile2 : kTile;
         double cand = (double)(all[t].i1 - all[t].i0) * d.K * outs;   // G1 items: kTile outputs too
         const double lanes = all[t].glog > 0 ? (double)(1 << (all[t].glog - d.glog)) : 1.0;   // wave tail
-        tdur[t] = 3.0 + cand / (3000.0 * lanes);
+        const int f = dur_family(d);
+        tdur[t] = dm.a[f] + cand / (dm.rate[f] * lanes);
     }
     std::vector<double> vtime(n, 0.0);
     for (int i = n - 1; i >= 0; --i) {                 // parents have higher ranks
