@@ -25,6 +25,12 @@ KEYS = [
     ("smsp__pcsamp_warps_issue_stalled_short_scoreboard", "stall short_sb"),
     ("smsp__pcsamp_warps_issue_stalled_lg_throttle", "stall lg_thr"),
     ("smsp__pcsamp_warps_issue_stalled_no_instructions", "stall no_inst"),
+    ("smsp__pcsamp_warps_issue_stalled_membar", "stall membar"),
+    ("smsp__pcsamp_warps_issue_stalled_barrier", "stall barrier"),
+    ("smsp__pcsamp_warps_issue_stalled_branch_resolving", "stall branch"),
+    ("smsp__pcsamp_warps_issue_stalled_mio_throttle", "stall mio"),
+    ("smsp__pcsamp_warps_issue_stalled_sleeping", "stall sleeping"),
+    ("smsp__pcsamp_warps_issue_stalled_drain", "stall drain"),
     ("smsp__pcsamp_warps_issue_stalled_selected", "selected"),
 ]
 
