@@ -215,6 +215,17 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
         const int f = dur_family(d);
         tdur[t] = dm.a[f] + cand / (dm.rate[f] * lanes);
     }
+    // A/B only (PASE_DUR_FILE): measured per-task durations (us, float64 per task in task-id
+    // order, e.g. from a PASE_TRACE timeline of the same plan) replace the model
+    if (const char* df = std::getenv("PASE_DUR_FILE")) {
+        if (FILE* fp = std::fopen(df, "rb")) {
+            std::vector<double> m((size_t)ntk);
+            if (std::fread(m.data(), sizeof(double), m.size(), fp) == m.size())
+                for (int64_t t = 0; t < ntk; ++t)
+                    if (all[t].vtx < n && m[t] > 0) tdur[t] = m[t];
+            std::fclose(fp);
+        }
+    }
     std::vector<double> vtime(n, 0.0);
     for (int i = n - 1; i >= 0; --i) {                 // parents have higher ranks
         double work = 0.0, longest = 0.0;

@@ -23,6 +23,10 @@ VARIANTS = {
     "streaming_no_tma": {"PASE_STREAM_MB": "0", "PASE_STREAM_TMA": "0"},   # ... or plain full-warp 1-D tile
     "ready_queue": {"PASE_QUEUE": "1"},                   # ready-queue claiming instead of the static order
     "cta_gate": {"PASE_EARLY_GATE": "0"},                 # one thread per CTA waits before the tile
+    "elected_gate_no_warm": {"PASE_GATE_ELECT": "1", "PASE_WARM": "0"},   # one poller per CTA, no warm pass
+    "task_length_cap": {"PASE_MAX_LANE_CAND": "64"},      # every big vertex widened (more, shorter tasks)
+    "fitted_durations": {"PASE_DUR": "1:3.4:2500,2:4:9000,3:3.3:3500,4:5:8500"},   # another claim order
+    "cta_tile": {"PASE_CTA": "1"},                        # CTA-tiled min-plus for the big vertices
 }
 
 
