@@ -5,7 +5,7 @@ import re
 import subprocess
 import sys
 
-so = "paper_2407_04001_b200/libpase.so"
+so = __import__("os").environ.get("SO", "paper_2407_04001_b200/libpase.so")
 subprocess.run(["cuobjdump", "-xelf", "kernels.sm_100a.cubin", so], cwd="/tmp", capture_output=True)
 L = subprocess.run(["nvdisasm", "-c", "/tmp/kernels.sm_100a.cubin"], capture_output=True, text=True).stdout.split("\n")
 want, kern = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "dp_persistent"
