@@ -459,7 +459,18 @@ int early_gate() {
         if (e && e[0] == '0') return 0;
         const char* w = std::getenv("PASE_WARM");
         const char* el = std::getenv("PASE_GATE_ELECT");
-        return ((w && w[0] == '0') ? 1 : 3) | ((el && el[0] == '1') ? 4 : 0);
+        // bits 3 / 4: acquire by ld.acquire of the counter instead of fence.acq_rel at the gates of
+        // 1-D tiles (PASE_GATE_LDACQ=1) / of every tile (2, the default: no MEMBAR.GPU per gate;
+        // same-binary A/B, profiles/r02_ab_reentry.txt: -4 % DP on Transformer, -6..-12 % on
+        // GNMT / RNNLM / InceptionV3 / AlexNet, -0.7 % on LE_P); 0 = the fence everywhere
+        const char* la = std::getenv("PASE_GATE_LDACQ");
+        const int ldacq = la ? std::atoi(la) : 2;
+        // bit 5 (default; PASE_REL_RED=0 turns it off): a finished task releases its parent with
+        // red.release (no return value to wait for) instead of atom.acq_rel -- its CTA claims the
+        // next task ~1 us sooner (same-binary A/B: -0.9 % DP on Transformer, -1.4 % GNMT, +0.8 % RNNLM)
+        const char* rr = std::getenv("PASE_REL_RED");
+        return ((w && w[0] == '0') ? 1 : 3) | ((el && el[0] == '1') ? 4 : 0) | (ldacq == 1 ? 8 : ldacq == 2 ? 16 : 0) |
+               ((rr && rr[0] == '0') ? 0 : 32);
     }();
     return mode;
 }

@@ -321,6 +321,7 @@ struct Gate {
                                  // its gate polls the global counter and opens a shared flag the
                                  // other warps spin on (one global poller per CTA instead of 8)
     int64_t* stamp;              // PASE_TRACE: per-warp {counter seen at 0, fence done} (ns)
+    int ldacq;                   // acquire by ld.acquire of the counter instead of fence.acq_rel
     int warm;                    // CTA-uniform: the children were still running when the task was
                                  // claimed -- run the first work item once WITHOUT stores before the
                                  // gate (warms this SM's instruction caches with the tile's code
@@ -365,6 +366,7 @@ __device__ __forceinline__ void gate_wait(Gate& g) {
         if (g.stamp) g.stamp[2 * (threadIdx.x >> 5)] = (int64_t)gate_clock();
         if (g.multi) { int v; asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(g.p) : "memory"); (void)v; }
         else if (PASE_GATE_LDACQ) { int v; asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(g.p) : "memory"); (void)v; }
+        else if (g.ldacq) { int v; asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(g.p) : "memory"); (void)v; }
         else asm volatile("fence.acq_rel.gpu;" ::: "memory");
         if (poller && g.elect) st_shared_relaxed(g.elect + 1, 1);
         if (g.stamp) g.stamp[2 * (threadIdx.x >> 5) + 1] = (int64_t)gate_clock();
@@ -1518,7 +1520,7 @@ dp_fill_vertex(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ 
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     run_shape(vd.shape, vd, td, tds, warp, nwarps, 0, vd.shape >= 0 ? vd.nitems : vd.nout, red_b, red_c, dyn, seq,
-              Gate{nullptr, nullptr, 0, 0, nullptr, nullptr, 0});
+              Gate{nullptr, nullptr, 0, 0, nullptr, nullptr, 0, 0});
 }
 
 void launch_dp_vertex(const VertexDesc* vd_dev, const TermDesc* td_dev, int vertex,
@@ -1729,6 +1731,7 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
         const Gate gate{(early_gate && !queue) ? pending + tk.vtx : nullptr, err, timeout_ns, multi ? 1 : 0,
                         (early_gate & 4) ? s_elect : nullptr,
                         trace ? trace + (int64_t)kTraceWords * task + kTraceTaskWords : nullptr,
+                        ((early_gate & 16) || ((early_gate & 8) && shape >= 0 && shape < kShape2D)) ? 1 : 0,
                         (early_gate && !queue) ? s_warm : 0};
         if (gate.stamp && (threadIdx.x & 31) == 0) gate.stamp[2 * warp] = gate.stamp[2 * warp + 1] = 0;
         run_shape(shape, vd, td, tds, warp, nwarps, tk.i0, tk.i1, red_b, red_c, dyn, seq, gate);
@@ -1768,7 +1771,7 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
                     for (int q = 0; q < peers.world; ++q) red_add_release_sys(peers.pending[q] + vd.parent, -1);
                 } else if (multi) {
                     red_add_release_sys(pending + vd.parent, -1);
-                } else if (PASE_REL_RED) {
+                } else if (PASE_REL_RED || (early_gate & 32)) {   // runtime A/B: PASE_REL_RED=1
                     red_add_release_gpu(pending + vd.parent, -1);
                 } else {
                     atom_add_acq_rel(pending + vd.parent, -1);

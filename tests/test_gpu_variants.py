@@ -27,6 +27,9 @@ VARIANTS = {
     "task_length_cap": {"PASE_MAX_LANE_CAND": "64"},      # every big vertex widened (more, shorter tasks)
     "fitted_durations": {"PASE_DUR": "1:3.4:2500,2:4:9000,3:3.3:3500,4:5:8500"},   # another claim order
     "cta_tile": {"PASE_CTA": "1"},                        # CTA-tiled min-plus for the big vertices
+    "gate_fence": {"PASE_GATE_LDACQ": "0"},               # gates acquire by fence.acq_rel (round-1 form)
+    "gate_ldacq_1d": {"PASE_GATE_LDACQ": "1"},            # ld.acquire at 1-D tile gates only
+    "release_atom": {"PASE_REL_RED": "0"},                # releases by atom.acq_rel (round-1 form)
 }
 
 
