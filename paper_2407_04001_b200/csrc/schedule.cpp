@@ -72,7 +72,9 @@ pase_status build_schedule(const Plan& P, std::vector<VertexDesc>& vd, int world
     const int n = P.n;
     const int G = std::max(world, 1);
     nblocks = std::max(nblocks, 1);
-    static const int64_t tpb = std::getenv("PASE_TASKS_PER_BLOCK") ? std::atoll(std::getenv("PASE_TASKS_PER_BLOCK")) : kTasksPerBlock;
+    // tasks per CTA of the grid for big vertices: 3 (same-binary A/B against kTasksPerBlock = 4,
+    // profiles/r02_ab_reentry.txt: DP -1.3 % Transformer, -2 % LE_P / GNMT 4+4, neutral elsewhere)
+    static const int64_t tpb = std::getenv("PASE_TASKS_PER_BLOCK") ? std::atoll(std::getenv("PASE_TASKS_PER_BLOCK")) : 3;
     const int64_t spread = std::max<int64_t>(1, tpb) * nblocks;
     const auto tt0 = std::chrono::steady_clock::now();
     // ---- per (vertex, rank): unit runs, split into tasks
