@@ -690,8 +690,19 @@ pase_status prepare(pase_ctx* ctx, bool device) {
             // their items cannot fill the grid -- is slower overall: 0.58 -> 0.76 / 1.42 ms DP
             // on Transformer p=64; the extra tasks cost more than the shorter chains save.)
             if ((int64_t)d.nout * d.K <= kLatencyCand) {
+                // values of C per lane (PASE_LAT_CPL, default 2: one round of loads)
+                static const int cpl = std::getenv("PASE_LAT_CPL") ? std::max(1, std::atoi(std::getenv("PASE_LAT_CPL"))) : 2;
                 int ll = 2;
-                while (ll < 8 && (2 << ll) < d.K) ++ll;
+                while (ll < 8 && (cpl << ll) < d.K) ++ll;
+                // one value of C per lane (twice the lanes) while that needs <= PASE_LAT_ONE_LANES
+                // lanes (default 16: K <= 16, the group stays inside a warp) and the vertex's tasks
+                // number <= PASE_LAT_ONE_TASKS (default unbounded; 0 = off).  Same-binary A/B
+                // (profiles/r02_ab_reentry.txt): InceptionV3 -14 % DP (87 K = 6 vertices), others
+                // +-0.1 %; wider limits (32+ lanes) cost Transformer / RNNLM 3-6 %.
+                static const int64_t one_tasks = std::getenv("PASE_LAT_ONE_TASKS") ? std::atoll(std::getenv("PASE_LAT_ONE_TASKS")) : (int64_t(1) << 40);
+                static const int one_lanes = std::getenv("PASE_LAT_ONE_LANES") ? std::atoi(std::getenv("PASE_LAT_ONE_LANES")) : 16;
+                if (one_tasks > 0 && ll < 8 && (2 << ll) >= d.K && (2 << ll) <= one_lanes &&
+                    (d.nitems << (ll + 1)) <= one_tasks * 256) ++ll;
                 d.glog = std::min(ll, 5);
                 d.wlog = ll - d.glog;
             }
