@@ -319,7 +319,8 @@ void widen_critical(pase_ctx* ctx) {
         bool changed = false;
         for (int i = 0; i < n; ++i) {
             VertexDesc& d = ctx->vd[i];
-            if (top[i] + bot[i] - w[i] < 0.85 * cp || d.shape < 0 || d.shape >= pase::kShapeG1 || d.wlog != 0) continue;
+            static const double crit = std::getenv("PASE_CRIT_FRAC") ? std::atof(std::getenv("PASE_CRIT_FRAC")) : 0.85;
+            if (top[i] + bot[i] - w[i] < crit * cp || d.shape < 0 || d.shape >= pase::kShapeG1 || d.wlog != 0) continue;
             while (d.glog < 5 && (widen_minc(d.K) << (d.glog + 1)) <= d.K && tasks_of(d) < nb) {
                 // a short reduction (K <= 64) is widened only while its tasks still fit one wave
                 if (d.K <= 64) {
@@ -442,7 +443,8 @@ void try_tile2(pase_ctx* ctx, VertexDesc& d, const TermDesc* tv, int top) {
     for (int t = d.tstar; t < d.nterms; ++t) l2 += tv[t].stride[q2] ? pase::kTile1 * pase::kTile2 : pase::kTile1;
     const double per2 = l2 / (pase::kTile1 * pase::kTile2);
     const double per1 = (double)(d.tstar + pase::kTile * NS) / pase::kTile;
-    if (per2 > 0.8 * per1) return;
+    static const double gain2 = std::getenv("PASE_2D_GAIN") ? std::atof(std::getenv("PASE_2D_GAIN")) : 0.8;
+    if (per2 > gain2 * per1) return;
     set_tile2(d, q2, f2);
     d.shape = pase::kShape2D + (NS - 1) * 4 + (d.glog - 2);
 }

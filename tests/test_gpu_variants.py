@@ -30,6 +30,7 @@ VARIANTS = {
     "gate_fence": {"PASE_GATE_LDACQ": "0"},               # gates acquire by fence.acq_rel (round-1 form)
     "gate_ldacq_1d": {"PASE_GATE_LDACQ": "1"},            # ld.acquire at 1-D tile gates only
     "release_atom": {"PASE_REL_RED": "0"},                # releases by atom.acq_rel (round-1 form)
+    "latency_two_c_per_lane": {"PASE_LAT_ONE_TASKS": "0"},   # no one-C-per-lane latency groups
 }
 
 
