@@ -30,6 +30,9 @@ constexpr int kCUnroll = PASE_CUNROLL;
 #ifndef PASE_GATE_LDACQ
 #define PASE_GATE_LDACQ 0      // per-warp gate: acquire via ld.acquire of the counter instead of a fence
 #endif
+#ifndef PASE_LAYOUT_PAD
+#define PASE_LAYOUT_PAD 0      // dead-code pad in dp_persistent (code placement A/B)
+#endif
 #ifndef PASE_REL_RED
 #define PASE_REL_RED 0         // release via red.release (no return) instead of atom.acq_rel
 #endif
@@ -1640,6 +1643,16 @@ dp_persistent(const VertexDesc* __restrict__ vds, const TermDesc* __restrict__ t
     // a group barrier that timed out (or any earlier failure of this solve) skips the DP: the
     // peers' tables may still be in use (the back-substitution skips its lookups too)
     if (ld_relaxed(err) != 0) return;
+#if PASE_LAYOUT_PAD > 0
+    // code-placement pad (build define; never executed: ntasks >= 0): shifts the placement of
+    // the tile functions that follow in the kernel's code (placement moves the DP by
+    // a few per cent between builds)
+    if (ntasks < 0) {
+#pragma unroll
+        for (int k = 0; k < PASE_LAYOUT_PAD; ++k)
+            asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_task)), "r"(k) : "memory");
+    }
+#endif
     for (;;) {
         int64_t t_claim = 0, t_start = 0;
         if (threadIdx.x == 0) {
